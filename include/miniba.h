@@ -1,0 +1,179 @@
+/*
+ * miniba.h -- C ABI of the B200-native mini bundle adjustment (libminiba.so).
+ *
+ * The reference (`/root/reference/pkg/src/gsrecon/miniba.py`) is a pure
+ * Python/numpy package with no FFI layer; its drop-in boundary is the Python
+ * surface of `gsrecon.miniba` that `pkg/smoke_miniba.py` imports. The Python
+ * host package `src/gsrecon` keeps that surface and binds these entry points
+ * with ctypes. Each entry point names the reference
+ * function it replaces.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers owned by the caller (torch
+ *    tensors on the Python side); the library never allocates on the hot path.
+ *  - float64 parameter state; int32 local indices; 16-byte observation records.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*).
+ *  - Return value: MBA_OK or a negative MbaStatus; per-problem solver
+ *    outcomes are data (MbaOutputs.status), not errors.
+ */
+#ifndef MINIBA_H_
+#define MINIBA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MBA_ABI_VERSION 1
+
+enum MbaStatus {
+  MBA_OK = 0,
+  MBA_ERR_INVALID = -1,     /* bad descriptor / argument (-> ValueError)          */
+  MBA_ERR_TOO_LARGE = -2,   /* problem exceeds the shared-memory plan             */
+  MBA_ERR_CUDA = -3,        /* CUDA launch / runtime failure                      */
+  MBA_ERR_EMPTY = -4,       /* a problem has no residuals (miniba.py:229-230)     */
+  MBA_ERR_NOT_PD = -5       /* stage solve: reduced system not PD (LinAlgError)   */
+};
+
+enum MbaLoss { MBA_LOSS_HUBER = 0, MBA_LOSS_CAUCHY = 1 };
+
+/* arithmetic of the linearise / Schur / Cholesky stages; state and the
+ * residual / cost passes are always float64 */
+enum MbaPrecision { MBA_LIN_F32 = 0, MBA_LIN_F64 = 1 };
+
+/* per-problem solver outcome (MbaOutputs.status) */
+enum MbaSolveStatus {
+  MBA_SOLVE_MAX_ITERS = 0,   /* ran max_iters iterations                        */
+  MBA_SOLVE_CONVERGED = 1,   /* improve <= 1e-15 max(cost,1)  (miniba.py:285)   */
+  MBA_SOLVE_LAMBDA_CAP = 2   /* rejected with lambda >= 1e10  (miniba.py:292)   */
+};
+
+/* One observation: pixel (u, v) rounded to float, local camera and point index.
+ * Within a problem the records are sorted point-major (all observations of
+ * point 0, then point 1, ...). */
+typedef struct {
+  float u, v;
+  int32_t cam;
+  int32_t pt;
+} MbaObs;
+
+/* A batch of independent problems, packed back to back (BaProblem,
+ * miniba.py:65-83). Offsets are int64 arrays of length n_problems + 1. */
+typedef struct {
+  int32_t n_problems;
+  int32_t max_cams;          /* max cameras in any problem            */
+  int64_t max_obs;           /* max observations in any problem       */
+  int64_t max_points;        /* max points in any problem             */
+  const int64_t* cam_off;    /* camera rows of problem b: [cam_off[b], cam_off[b+1]) */
+  const int64_t* pt_off;
+  const int64_t* obs_off;
+  const MbaObs* obs;         /* [total_obs]                                      */
+  const float* obs_lo;       /* [total_obs][2] uv - float(uv) (exact fp64 uv), or NULL */
+  const uint8_t* fixed;      /* [total_cams] 1 = fixed camera (miniba.py:78)     */
+  const double* cx;          /* [n_problems]                                      */
+  const double* cy;          /* [n_problems]                                      */
+  const uint8_t* flags;      /* [n_problems] bit0 optimize_focal, bit1 optimize_points */
+} MbaBatchDesc;
+
+/* LmConfig (config.py:9-17) plus the loss / precision extensions */
+typedef struct {
+  double lambda_init;
+  double nu;
+  double delta;              /* Huber delta / Cauchy scale, px            */
+  int32_t max_iters;
+  int32_t loss;              /* MbaLoss                                   */
+  int32_t precision;         /* MbaPrecision                              */
+  int32_t ctas_per_problem;  /* 0 = auto; >1 = thread-block cluster per problem */
+  uint64_t fail_iters_mask;  /* fault injection (tests): bit i forces the solve of
+                                iteration i to fail like a LinAlgError (miniba.py:247-251) */
+} MbaLmConfig;
+
+/* Parameter state in / out and the LM traces (lm_solve return dict,
+ * miniba.py:294-296). *_in may alias *_out. */
+typedef struct {
+  const double* R_in;        /* [total_cams][3][3] */
+  const double* t_in;        /* [total_cams][3]    */
+  const double* focal_in;    /* [n_problems]       */
+  const double* points_in;   /* [total_points][3]  */
+  double* R_out;
+  double* t_out;
+  double* focal_out;
+  double* points_out;
+  double* costs;             /* [n_problems][max_iters+1] robust cost trace      */
+  double* lambdas;           /* [n_problems][max_iters]                          */
+  uint8_t* accepted;         /* [n_problems][max_iters]                          */
+  uint8_t* evals;            /* [n_problems][max_iters] trial passes executed    */
+  int32_t* n_iters;          /* [n_problems]                                     */
+  int32_t* status;           /* [n_problems] MbaSolveStatus                      */
+  double* final_stats;       /* [n_problems][4]: cost, sum e, sum e^2, K         */
+} MbaOutputs;
+
+int32_t mba_abi_version(void);
+
+/* Bytes of device workspace mba_solve needs for this batch and config. */
+size_t mba_workspace_bytes(const MbaBatchDesc* desc, const MbaLmConfig* cfg);
+
+/* Full Levenberg-Marquardt mini-BA on every problem of the batch: replaces
+ * lm_solve (miniba.py:223-296) with its helpers residuals (85-98),
+ * huber_cost/weights (46-54), _build_blocks (101-132), _assemble (135-177)
+ * and solve_step(method="schur") (180-220). The whole LM loop runs on device;
+ * no host round trip per iteration. */
+int32_t mba_solve(const MbaBatchDesc* desc, const MbaLmConfig* cfg, const MbaOutputs* out,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- stage entry points (float64), for the reference's internal API ---- */
+
+/* BaProblem.residuals (miniba.py:85-98): r [K][2], p_cam [K][3], bad [K] */
+int32_t mba_residuals(int64_t K, const double* R, const double* t, double focal, double cx,
+                      double cy, const double* points, const int64_t* cam_idx,
+                      const int64_t* pt_idx, const double* uv, double* r, double* p_cam,
+                      uint8_t* bad, void* stream);
+
+/* huber_cost / huber_weights (miniba.py:46-54) and the Cauchy extension:
+ * w [n] (may be NULL) and the summed cost into cost[0] (may be NULL). */
+int32_t mba_robust(int64_t n, const double* e, double delta, int32_t loss, double* w,
+                   double* cost, void* stream);
+
+/* _build_blocks (miniba.py:101-132): A [K][2][6], F [K][2], B [K][2][3] */
+int32_t mba_blocks(int64_t K, const double* R, const double* t, double focal,
+                   const int64_t* cam_idx, const double* p_cam, const uint8_t* bad, double* A,
+                   double* F, double* B, void* stream);
+
+/* _assemble (miniba.py:135-177). Observation orders are supplied by the
+ * caller: pt_order/pt_ptr (observations grouped by point, P+1 offsets) and
+ * cam_order/cam_ptr (grouped by camera, n+1 offsets); slot[n_cams] maps a
+ * camera to its free-camera slot (-1 = fixed), cam_of_slot[n_free] inverts it.
+ * Outputs dense U [C][C], g_c [C], V [P][3][3], g_p [P][3], Wf [P][C][3]
+ * (zeroed by the call). */
+int32_t mba_assemble(int64_t K, int32_t n_cams, int32_t n_free, int64_t P, const int32_t* slot,
+                     const int32_t* cam_of_slot, int32_t optimize_focal, int32_t optimize_points,
+                     const int64_t* cam_idx, const double* w, const double* r, const double* A,
+                     const double* F, const double* B, const int64_t* pt_order,
+                     const int64_t* pt_ptr, const int64_t* cam_order, const int64_t* cam_ptr,
+                     double* U, double* g_c, double* V, double* g_p, double* Wf, void* stream);
+
+/* solve_step (miniba.py:180-220); method 0 = schur, 1 = dense. Writes dc [C],
+ * dp [P][3]. `scratch` must hold mba_solve_step_scratch_bytes(C, P, method).
+ * Returns MBA_ERR_NOT_PD when the factorisation fails (np.linalg.LinAlgError). */
+size_t mba_solve_step_scratch_bytes(int32_t C, int64_t P, int32_t method);
+int32_t mba_solve_step(int32_t C, int64_t P, const double* U, const double* g_c,
+                       const double* V, const double* g_p, const double* Wf, double lam,
+                       int32_t method, double* dc, double* dp, void* scratch, void* stream);
+
+/* Batched pose-only LM (pose_lm, miniba.py:334-389): nb problems of m
+ * correspondences each, `iters` single-trial iterations. R/t updated in
+ * place; cost [nb]. If X_all/uv_all are given, also scores every refined
+ * hypothesis on the full correspondence set (estimate_pose_ransac,
+ * miniba.py:418-431): inlier count [nb] and inlier sum of squared errors [nb]. */
+int32_t mba_pose_lm(int32_t nb, int32_t m, const double* X, const double* uv, double focal,
+                    double cx, double cy, int32_t iters, double lambda_init, double nu,
+                    double delta, double* R, double* t, double* cost, int32_t m_all,
+                    const double* X_all, const double* uv_all, double inlier_px,
+                    int32_t* inliers, double* inlier_sse, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MINIBA_H_ */

@@ -1,0 +1,759 @@
+// mba_solve.cu -- on-device Levenberg-Marquardt mini bundle adjustment (sm_100a).
+//
+// Replaces lm_solve (miniba.py:223-296) and, inside it, residuals (85-98),
+// huber_cost/weights (46-54), _build_blocks (101-132), _assemble (135-177) and
+// solve_step(method="schur") (180-220).
+//
+// Execution model: a persistent grid; each CTA pulls whole problems from an
+// atomic work counter and runs the complete LM loop for that problem on chip:
+//
+//   setup      point CSR (binary search), camera-major permutation (warp ballots)
+//   cost pass  one thread per observation, 16-byte record loads, fp64 residual
+//              and robust cost, deterministic block reduction
+//   per iteration:
+//     K1+K2  point pass    one thread per point: fp64 residuals, Jacobians in
+//                          T (float or double), V_p / g_p / W_i accumulation in
+//                          registers, 3x3 Cholesky of the damped V_p, and the
+//                          Schur factors Y_i = W_i L_p^-T, z_p, y_f (K3 prep)
+//     K2     camera jobs   one warp per free camera: U_cc, U_cf, g_c
+//     K3     pair jobs     one warp per camera pair (a<=b): S_ab -= sum Y_i Y_j^T
+//                          (all reductions are fixed-order warp butterflies;
+//                          no atomics, bit-reproducible)
+//     K4     Cholesky      packed reduced camera system in shared memory,
+//                          forward/back substitution for dc
+//            back-sub      dp_p = -L_p^-T (z_p + sum Y_i^T dc + y_f df)
+//     K5     trials        <= 5 backtracking cost passes (fp64), accept/reject,
+//                          lambda schedule and termination -- all on device
+//
+// State (cameras, focal, points) is float64; T selects the arithmetic of the
+// linearise/Schur/Cholesky stages (mixed-precision iterative refinement when
+// T = float, SURVEY 8c design (b)).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "mba_common.cuh"
+
+namespace mba {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kPtStride = 16;   // per-point workspace: L(6) z(3) yf(3) dp(3) pad
+constexpr int kYStride = 18;    // per-observation workspace: W_i then Y_i (6x3)
+constexpr int kUcamStride = 33; // per free camera: U_aa lower(21) U_af(6) g_a(6)
+
+struct SolveParams {
+  MbaBatchDesc d;
+  MbaLmConfig cfg;
+  MbaOutputs o;
+  int* counter;
+  unsigned char* ws;       // per-slot workspace base
+  size_t ws_slot_bytes;
+  int max_cams;
+};
+
+template <typename T>
+struct Smem {
+  double* Rc;   // [n][9] current rotations
+  double* tc;   // [n][3]
+  double* Rt;   // [n][9] trial
+  double* tt;   // [n][3]
+  double* dc;   // [Cmax] step (double copy)
+  double* red;  // [kWarps * 4]
+  T* S;         // packed lower [Cmax(Cmax+1)/2]
+  T* rhs;       // [Cmax]
+  T* ucam;      // [nfmax * 33]
+  T* pairf;     // [nfmax * 12]
+  int* cam_ptr; // [n+1]
+  int* slot;    // [n]
+  int* cam_of_slot;  // [n]
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+template <typename T>
+__host__ __device__ inline size_t smem_bytes(int max_cams) {
+  size_t n = max_cams, C = 6 * n + 1;
+  size_t b = 0;
+  b += align16(sizeof(double) * n * 24);
+  b += align16(sizeof(double) * C);
+  b += align16(sizeof(double) * kWarps * 4);
+  b += align16(sizeof(T) * C * (C + 1) / 2);
+  b += align16(sizeof(T) * C);
+  b += align16(sizeof(T) * n * kUcamStride);
+  b += align16(sizeof(T) * n * 12);
+  b += align16(sizeof(int) * (n + 1));
+  b += align16(sizeof(int) * n * 2);
+  return b;
+}
+
+template <typename T>
+__device__ inline Smem<T> carve(unsigned char* base, int max_cams) {
+  Smem<T> s;
+  size_t n = max_cams, C = 6 * n + 1, off = 0;
+  auto take = [&](size_t bytes) { unsigned char* p = base + off; off += align16(bytes); return p; };
+  double* cams = (double*)take(sizeof(double) * n * 24);
+  s.Rc = cams;
+  s.tc = cams + 9 * n;
+  s.Rt = cams + 12 * n;
+  s.tt = cams + 21 * n;
+  s.dc = (double*)take(sizeof(double) * C);
+  s.red = (double*)take(sizeof(double) * kWarps * 4);
+  s.S = (T*)take(sizeof(T) * C * (C + 1) / 2);
+  s.rhs = (T*)take(sizeof(T) * C);
+  s.ucam = (T*)take(sizeof(T) * n * kUcamStride);
+  s.pairf = (T*)take(sizeof(T) * n * 12);
+  s.cam_ptr = (int*)take(sizeof(int) * (n + 1));
+  int* sl = (int*)take(sizeof(int) * n * 2);
+  s.slot = sl;
+  s.cam_of_slot = sl + n;
+  return s;
+}
+
+template <typename T>
+__host__ __device__ inline size_t ws_slot_bytes(int64_t max_obs, int64_t max_points) {
+  size_t b = 0;
+  b += align16(sizeof(int) * max_obs);              // camera-major permutation
+  b += align16(sizeof(int) * (max_points + 1));     // point CSR
+  b += align16(sizeof(T) * kYStride * max_obs);     // W_i / Y_i
+  b += align16(sizeof(T) * kPtStride * max_points); // per-point factors
+  return b;
+}
+
+struct Obs {
+  double u, v;
+  int cam, pt;
+};
+
+__device__ __forceinline__ Obs load_obs(const MbaObs* __restrict__ obs, const float* __restrict__ lo,
+                                        int64_t k) {
+  float4 r = __ldg(reinterpret_cast<const float4*>(obs) + k);
+  Obs o;
+  o.u = (double)r.x;
+  o.v = (double)r.y;
+  o.cam = __float_as_int(r.z);
+  o.pt = __float_as_int(r.w);
+  if (lo != nullptr) {
+    float2 l = __ldg(reinterpret_cast<const float2*>(lo) + k);
+    o.u += (double)l.x;
+    o.v += (double)l.y;
+  }
+  return o;
+}
+
+__device__ __forceinline__ int obs_cam(const MbaObs* __restrict__ obs, int64_t k) {
+  return __ldg(&obs[k].cam);
+}
+
+// Cost pass over all observations with camera set (Rs, ts, f) and points
+// X + frac * dp. Returns (sum rho, sum e, sum e^2) to every thread.
+template <typename T>
+__device__ void cost_pass(const MbaObs* __restrict__ obs, const float* __restrict__ lo, int K,
+                          const double* __restrict__ X, const T* __restrict__ ptw, double frac,
+                          bool use_dp, const double* Rs, const double* ts, double f, double cx,
+                          double cy, double delta, int loss, double* red, double out[3]) {
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    Obs o = load_obs(obs, lo, k);
+    double Xp[3] = {X[3 * o.pt + 0], X[3 * o.pt + 1], X[3 * o.pt + 2]};
+    if (use_dp) {
+      const T* dp = ptw + (size_t)o.pt * kPtStride + 12;
+      Xp[0] = Xp[0] + frac * (double)dp[0];
+      Xp[1] = Xp[1] + frac * (double)dp[1];
+      Xp[2] = Xp[2] + frac * (double)dp[2];
+    }
+    Proj pr = project_residual(Rs + 9 * o.cam, ts + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
+    double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
+    acc[0] += robust_rho(e, delta, loss);
+    acc[1] += e;
+    acc[2] += e * e;
+  }
+  block_sum<double, 3>(acc, red);
+  out[0] = acc[0];
+  out[1] = acc[1];
+  out[2] = acc[2];
+}
+
+template <typename T>
+__device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const MbaBatchDesc& D = P.d;
+  const MbaLmConfig& cfg = P.cfg;
+  const MbaOutputs& O = P.o;
+  Smem<T> sm = carve<T>(smem_raw, P.max_cams);
+  __shared__ int s_flag;        // setup error / Cholesky failure
+  __shared__ int s_C, s_nf;
+  __shared__ double s_red4[kWarps * 4];
+
+  const int64_t cb = D.cam_off[b], pb = D.pt_off[b], ob = D.obs_off[b];
+  const int n = (int)(D.cam_off[b + 1] - cb);
+  const int Pn = (int)(D.pt_off[b + 1] - pb);
+  const int K = (int)(D.obs_off[b + 1] - ob);
+  const uint8_t fl = D.flags[b];
+  const bool has_f = fl & 1, opt_pts = (fl >> 1) & 1;
+  const double cx = D.cx[b], cy = D.cy[b];
+  const double delta = cfg.delta, nu = cfg.nu;
+  const int loss = cfg.loss, max_it = cfg.max_iters;
+  const MbaObs* __restrict__ obs = D.obs + ob;
+  const float* __restrict__ lo = D.obs_lo ? D.obs_lo + 2 * ob : nullptr;
+  double* __restrict__ X = O.points_out + 3 * pb;
+
+  unsigned char* ws = P.ws + (size_t)blockIdx.x * P.ws_slot_bytes;
+  int* perm = (int*)ws;
+  int* ptr = (int*)(ws + align16(sizeof(int) * D.max_obs));
+  T* Ybuf = (T*)((unsigned char*)ptr + align16(sizeof(int) * (D.max_points + 1)));
+  T* ptw = (T*)((unsigned char*)Ybuf + align16(sizeof(T) * kYStride * D.max_obs));
+
+  double* costs = O.costs + (size_t)b * (max_it + 1);
+  double* lambdas = O.lambdas + (size_t)b * max_it;
+  uint8_t* accepted = O.accepted + (size_t)b * max_it;
+  uint8_t* evals = O.evals + (size_t)b * max_it;
+
+  // ---------------- setup ----------------
+  for (int i = tid; i < n * 9; i += blockDim.x) sm.Rc[i] = O.R_in[cb * 9 + i];
+  for (int i = tid; i < n * 3; i += blockDim.x) sm.tc[i] = O.t_in[cb * 3 + i];
+  if (O.points_in != O.points_out)
+    for (int i = tid; i < Pn * 3; i += blockDim.x) X[i] = O.points_in[pb * 3 + i];
+  if (tid == 0) {
+    int nf = 0;
+    for (int c = 0; c < n; ++c) {
+      if (D.fixed[cb + c]) {
+        sm.slot[c] = -1;
+      } else {
+        sm.slot[c] = nf;
+        sm.cam_of_slot[nf] = c;
+        ++nf;
+      }
+    }
+    s_nf = nf;
+    s_C = 6 * nf + (has_f ? 1 : 0);
+    s_flag = 0;
+  }
+  // point CSR: obs are point-major; ptr[p] = first k with pt >= p
+  for (int p = tid; p <= Pn; p += blockDim.x) {
+    int lo_i = 0, hi_i = K;
+    while (lo_i < hi_i) {
+      int mid = (lo_i + hi_i) >> 1;
+      if (__ldg(&obs[mid].pt) < p) lo_i = mid + 1; else hi_i = mid;
+    }
+    ptr[p] = lo_i;
+  }
+  // validate ordering and index ranges
+  for (int k = tid; k < K; k += blockDim.x) {
+    int pt = __ldg(&obs[k].pt), c = __ldg(&obs[k].cam);
+    bool bad = pt < 0 || pt >= Pn || c < 0 || c >= n || (k > 0 && __ldg(&obs[k - 1].pt) > pt);
+    if (bad) s_flag = 1;
+  }
+  __syncthreads();
+  // camera-major permutation: warp per camera, two ballot sweeps
+  for (int c = wid; c < n; c += kWarps) {
+    int cnt = 0;
+    for (int k0 = 0; k0 < K; k0 += 32) {
+      int k = k0 + lane;
+      bool hit = k < K && obs_cam(obs, k) == c;
+      cnt += __popc(__ballot_sync(0xffffffffu, hit));
+    }
+    if (lane == 0) sm.cam_ptr[c + 1] = cnt;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    sm.cam_ptr[0] = 0;
+    for (int c = 0; c < n; ++c) sm.cam_ptr[c + 1] += sm.cam_ptr[c];
+  }
+  __syncthreads();
+  for (int c = wid; c < n; c += kWarps) {
+    int base = sm.cam_ptr[c];
+    for (int k0 = 0; k0 < K; k0 += 32) {
+      int k = k0 + lane;
+      bool hit = k < K && obs_cam(obs, k) == c;
+      unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (hit) perm[base + __popc(m & ((1u << lane) - 1u))] = k;
+      base += __popc(m);
+    }
+  }
+  const int nf = s_nf, C = s_C, FI = C - 1;
+  double f = O.focal_in[b];
+  if (s_flag) {  // malformed problem: report and leave parameters untouched
+    if (tid == 0) {
+      O.n_iters[b] = 0;
+      O.status[b] = -1;
+      if (O.focal_out) O.focal_out[b] = f;
+    }
+    for (int i = tid; i < n * 9; i += blockDim.x) O.R_out[cb * 9 + i] = sm.Rc[i];
+    for (int i = tid; i < n * 3; i += blockDim.x) O.t_out[cb * 3 + i] = sm.tc[i];
+    __syncthreads();
+    return;
+  }
+  __syncthreads();
+
+  // initial cost (miniba.py:232-235)
+  double st[3];
+  cost_pass<T>(obs, lo, K, X, ptw, 0.0, false, sm.Rc, sm.tc, f, cx, cy, delta, loss, sm.red, st);
+  double cost = st[0], se = st[1], se2 = st[2];
+  double lam = cfg.lambda_init;
+  if (tid == 0) costs[0] = cost;
+  int it = 0, stop_reason = MBA_SOLVE_MAX_ITERS;
+
+  for (; it < max_it;) {
+    const T tlam = T(lam);
+    // ---------- K1+K2 point pass ----------
+    T part[4] = {T(0), T(0), T(0), T(0)};  // U_ff, g_f, sum yf.yf, sum yf.z
+    for (int p = tid; p < Pn; p += blockDim.x) {
+      const double Xp[3] = {X[3 * p], X[3 * p + 1], X[3 * p + 2]};
+      const int k0 = ptr[p], k1 = ptr[p + 1];
+      T V[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};  // 00 10 11 20 21 22
+      T g[3] = {T(0), T(0), T(0)}, wf[3] = {T(0), T(0), T(0)};
+      for (int k = k0; k < k1; ++k) {
+        Obs o = load_obs(obs, lo, k);
+        const double* Rk = sm.Rc + 9 * o.cam;
+        Proj pr = project_residual(Rk, sm.tc + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
+        double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
+        T w = T(robust_w(e, delta, loss));
+        T A[12], Fb[2], Bm[6];
+        jac_blocks<T>(pr, Rk, f, A, Fb, Bm);
+        T r0 = T(pr.ru), r1 = T(pr.rv);
+        T wB[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) wB[i] = w * Bm[i];
+        if (has_f) {
+          part[0] += w * (Fb[0] * Fb[0] + Fb[1] * Fb[1]);
+          part[1] += w * (Fb[0] * r0 + Fb[1] * r1);
+        }
+        if (opt_pts) {
+          V[0] += Bm[0] * wB[0] + Bm[3] * wB[3];
+          V[1] += Bm[1] * wB[0] + Bm[4] * wB[3];
+          V[2] += Bm[1] * wB[1] + Bm[4] * wB[4];
+          V[3] += Bm[2] * wB[0] + Bm[5] * wB[3];
+          V[4] += Bm[2] * wB[1] + Bm[5] * wB[4];
+          V[5] += Bm[2] * wB[2] + Bm[5] * wB[5];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) g[a] += wB[a] * r0 + wB[3 + a] * r1;
+          if (has_f) {
+            T wf0 = w * Fb[0], wf1 = w * Fb[1];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) wf[a] += wf0 * Bm[a] + wf1 * Bm[3 + a];
+          }
+          if (sm.slot[o.cam] >= 0) {
+            T* Wk = Ybuf + (size_t)k * kYStride;
+#pragma unroll
+            for (int r = 0; r < 6; ++r)
+#pragma unroll
+              for (int a = 0; a < 3; ++a) Wk[r * 3 + a] = A[r] * wB[a] + A[6 + r] * wB[3 + a];
+          }
+        }
+      }
+      if (!opt_pts) continue;
+      // damping (miniba.py:191-193) and 3x3 Cholesky of Vd
+      V[0] += tlam * (V[0] > T(kDiagFloor) ? V[0] : T(kDiagFloor));
+      V[2] += tlam * (V[2] > T(kDiagFloor) ? V[2] : T(kDiagFloor));
+      V[5] += tlam * (V[5] > T(kDiagFloor) ? V[5] : T(kDiagFloor));
+      T L00 = sqrt(V[0]);
+      T i00 = T(1) / L00;
+      T L10 = V[1] * i00, L20 = V[3] * i00;
+      T L11 = sqrt(V[2] - L10 * L10);
+      T i11 = T(1) / L11;
+      T L21 = (V[4] - L20 * L10) * i11;
+      T L22 = sqrt(V[5] - L20 * L20 - L21 * L21);
+      T i22 = T(1) / L22;
+      for (int k = k0; k < k1; ++k) {
+        if (sm.slot[obs_cam(obs, k)] < 0) continue;
+        T* Wk = Ybuf + (size_t)k * kYStride;
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+          T y0 = Wk[r * 3 + 0] * i00;
+          T y1 = (Wk[r * 3 + 1] - L10 * y0) * i11;
+          T y2 = (Wk[r * 3 + 2] - L20 * y0 - L21 * y1) * i22;
+          Wk[r * 3 + 0] = y0;
+          Wk[r * 3 + 1] = y1;
+          Wk[r * 3 + 2] = y2;
+        }
+      }
+      T z0 = g[0] * i00, z1 = (g[1] - L10 * z0) * i11, z2 = (g[2] - L20 * z0 - L21 * z1) * i22;
+      T f0 = wf[0] * i00, f1 = (wf[1] - L10 * f0) * i11, f2 = (wf[2] - L20 * f0 - L21 * f1) * i22;
+      part[2] += f0 * f0 + f1 * f1 + f2 * f2;
+      part[3] += f0 * z0 + f1 * z1 + f2 * z2;
+      T* pw = ptw + (size_t)p * kPtStride;
+      pw[0] = L00; pw[1] = L10; pw[2] = L11; pw[3] = L20; pw[4] = L21; pw[5] = L22;
+      pw[6] = z0; pw[7] = z1; pw[8] = z2;
+      pw[9] = f0; pw[10] = f1; pw[11] = f2;
+    }
+    {
+      double pd[4] = {(double)part[0], (double)part[1], (double)part[2], (double)part[3]};
+      if (sizeof(T) == 4) {
+        // float partials are reduced in float to keep the arithmetic of T
+        T pf[4] = {part[0], part[1], part[2], part[3]};
+        block_sum<T, 4>(pf, (T*)s_red4);
+        for (int i = 0; i < 4; ++i) pd[i] = (double)pf[i];
+      } else {
+        block_sum<double, 4>(pd, s_red4);
+      }
+      part[0] = T(pd[0]); part[1] = T(pd[1]); part[2] = T(pd[2]); part[3] = T(pd[3]);
+    }
+    // (block_sum ended with __syncthreads: point factors are visible)
+
+    // ---------- K2 camera jobs + K3 pair jobs (one warp per job) ----------
+    const int n_pair = opt_pts ? nf * (nf + 1) / 2 : 0;
+    for (int job = wid; job < nf + n_pair; job += kWarps) {
+      if (job < nf) {
+        const int s = job, c = sm.cam_of_slot[s];
+        const double* Rk = sm.Rc + 9 * c;
+        T acc[kUcamStride];
+#pragma unroll
+        for (int i = 0; i < kUcamStride; ++i) acc[i] = T(0);
+        for (int q = sm.cam_ptr[c] + lane; q < sm.cam_ptr[c + 1]; q += 32) {
+          const int k = perm[q];
+          Obs o = load_obs(obs, lo, k);
+          const double Xp[3] = {X[3 * o.pt], X[3 * o.pt + 1], X[3 * o.pt + 2]};
+          Proj pr = project_residual(Rk, sm.tc + 3 * c, Xp, f, cx, cy, o.u, o.v);
+          double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
+          T w = T(robust_w(e, delta, loss));
+          T A[12], Fb[2], Bm[6];
+          jac_blocks<T>(pr, Rk, f, A, Fb, Bm);
+          T r0 = T(pr.ru), r1 = T(pr.rv);
+          int idx = 0;
+#pragma unroll
+          for (int r = 0; r < 6; ++r) {
+            T wa0 = w * A[r], wa1 = w * A[6 + r];
+#pragma unroll
+            for (int cc = 0; cc <= r; ++cc) acc[idx++] += wa0 * A[cc] + wa1 * A[6 + cc];
+            acc[21 + r] += wa0 * Fb[0] + wa1 * Fb[1];
+            acc[27 + r] += wa0 * r0 + wa1 * r1;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < kUcamStride; ++i) acc[i] = warp_sum(acc[i]);
+        if (lane == 0)
+          for (int i = 0; i < kUcamStride; ++i) sm.ucam[s * kUcamStride + i] = acc[i];
+      } else {
+        // pair job index -> (sa <= sb)
+        int jj = job - nf, sa = 0;
+        while (jj >= nf - sa) { jj -= nf - sa; ++sa; }
+        const int sb = sa + jj;
+        const int ca = sm.cam_of_slot[sa], cbm = sm.cam_of_slot[sb];
+        const bool diag = sa == sb;
+        T acc[36], accf[6], accr[6];
+#pragma unroll
+        for (int i = 0; i < 36; ++i) acc[i] = T(0);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) accf[i] = accr[i] = T(0);
+        for (int q = sm.cam_ptr[ca] + lane; q < sm.cam_ptr[ca + 1]; q += 32) {
+          const int ki = perm[q];
+          const int pt = __ldg(&obs[ki].pt);
+          const T* Yi = Ybuf + (size_t)ki * kYStride;
+          T yi[18];
+#pragma unroll
+          for (int i = 0; i < 18; ++i) yi[i] = Yi[i];
+          const int j0 = ptr[pt], j1 = ptr[pt + 1];
+          for (int kj = j0; kj < j1; ++kj) {
+            if (obs_cam(obs, kj) != cbm) continue;
+            const T* Yj = Ybuf + (size_t)kj * kYStride;
+            T yj[18];
+#pragma unroll
+            for (int i = 0; i < 18; ++i) yj[i] = Yj[i];
+#pragma unroll
+            for (int r = 0; r < 6; ++r)
+#pragma unroll
+              for (int cc = 0; cc < 6; ++cc)
+                acc[r * 6 + cc] += yi[r * 3] * yj[cc * 3] + yi[r * 3 + 1] * yj[cc * 3 + 1] +
+                                   yi[r * 3 + 2] * yj[cc * 3 + 2];
+          }
+          if (diag) {
+            const T* pw = ptw + (size_t)pt * kPtStride;
+            T z0 = pw[6], z1 = pw[7], z2 = pw[8], f0 = pw[9], f1 = pw[10], f2 = pw[11];
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+              accf[r] += yi[r * 3] * f0 + yi[r * 3 + 1] * f1 + yi[r * 3 + 2] * f2;
+              accr[r] += yi[r * 3] * z0 + yi[r * 3 + 1] * z1 + yi[r * 3 + 2] * z2;
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 36; ++i) acc[i] = warp_sum(acc[i]);
+        if (diag) {
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            accf[i] = warp_sum(accf[i]);
+            accr[i] = warp_sum(accr[i]);
+          }
+        }
+        if (lane == 0) {
+          if (diag) {
+            for (int r = 0; r < 6; ++r)
+              for (int cc = 0; cc <= r; ++cc) sm.S[tri_idx(6 * sa + r, 6 * sa + cc)] = -acc[r * 6 + cc];
+            for (int i = 0; i < 6; ++i) {
+              sm.pairf[sa * 12 + i] = accf[i];
+              sm.pairf[sa * 12 + 6 + i] = accr[i];
+            }
+          } else {
+            // block (sa, sb) with sa < sb lives at rows of sb in the lower triangle
+            for (int r = 0; r < 6; ++r)
+              for (int cc = 0; cc < 6; ++cc) sm.S[tri_idx(6 * sb + r, 6 * sa + cc)] = -acc[cc * 6 + r];
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---------- assemble damped S and rhs (miniba.py:188-213) ----------
+    if (!opt_pts) {
+      for (int i = tid; i < C * (C + 1) / 2; i += blockDim.x) sm.S[i] = T(0);
+      for (int i = tid; i < nf * 12; i += blockDim.x) sm.pairf[i] = T(0);
+      __syncthreads();
+    }
+    for (int s = tid; s < nf; s += blockDim.x) {
+      const T* u = sm.ucam + s * kUcamStride;
+      int idx = 0;
+      for (int r = 0; r < 6; ++r) {
+        for (int cc = 0; cc <= r; ++cc, ++idx) {
+          T ud = u[idx];
+          if (r == cc) ud += tlam * (ud > T(kDiagFloor) ? ud : T(kDiagFloor));
+          sm.S[tri_idx(6 * s + r, 6 * s + cc)] += ud;
+        }
+        if (has_f) sm.S[tri_idx(FI, 6 * s + r)] = u[21 + r] - sm.pairf[s * 12 + r];
+        sm.rhs[6 * s + r] = -u[27 + r] + sm.pairf[s * 12 + 6 + r];
+      }
+      if (nf > 0 && s == 0) {
+        // off-diagonal camera blocks are pure Schur terms; zero them if points are fixed
+      }
+    }
+    if (has_f && tid == 0) {
+      T uff = part[0];
+      T ud = uff + tlam * (uff > T(kDiagFloor) ? uff : T(kDiagFloor));
+      sm.S[tri_idx(FI, FI)] = ud - part[2];
+      sm.rhs[FI] = -part[1] + part[3];
+    }
+    __syncthreads();
+
+    // ---------- K4 Cholesky of the reduced camera system ----------
+    for (int k = 0; k < C; ++k) {
+      if (tid == 0) {
+        T d = sm.S[tri_idx(k, k)];
+        if (!(d > T(0)) || !isfinite((double)d)) s_flag = 1;
+        else sm.S[tri_idx(k, k)] = sqrt(d);
+      }
+      __syncthreads();
+      if (s_flag) break;
+      const T dkk = sm.S[tri_idx(k, k)];
+      const T idkk = T(1) / dkk;
+      for (int i = k + 1 + tid; i < C; i += blockDim.x) sm.S[tri_idx(i, k)] *= idkk;
+      __syncthreads();
+      for (int i = k + 1 + wid; i < C; i += kWarps) {
+        const T lik = sm.S[tri_idx(i, k)];
+        T* row = sm.S + tri_idx(i, 0);
+        for (int j = k + 1 + lane; j <= i; j += 32) row[j] -= lik * sm.S[tri_idx(j, k)];
+      }
+      __syncthreads();
+    }
+    const bool chol_fail = s_flag != 0 || (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull));
+    __syncthreads();
+    if (tid == 0) s_flag = 0;
+
+    if (!chol_fail) {
+      // forward / back substitution in warp 0
+      if (wid == 0) {
+        for (int k = 0; k < C; ++k) {
+          T yk = sm.rhs[k] / sm.S[tri_idx(k, k)];
+          __syncwarp();
+          if (lane == 0) sm.rhs[k] = yk;
+          for (int i = k + 1 + lane; i < C; i += 32) sm.rhs[i] -= sm.S[tri_idx(i, k)] * yk;
+          __syncwarp();
+        }
+        for (int k = C - 1; k >= 0; --k) {
+          T xk = sm.rhs[k] / sm.S[tri_idx(k, k)];
+          __syncwarp();
+          if (lane == 0) sm.rhs[k] = xk;
+          const T* row = sm.S + tri_idx(k, 0);
+          for (int i = lane; i < k; i += 32) sm.rhs[i] -= row[i] * xk;
+          __syncwarp();
+        }
+        for (int i = lane; i < C; i += 32) sm.dc[i] = (double)sm.rhs[i];
+      }
+      __syncthreads();
+      // back substitution for the points (miniba.py:217)
+      if (opt_pts) {
+        const T df = has_f ? T(sm.dc[FI]) : T(0);
+        for (int p = tid; p < Pn; p += blockDim.x) {
+          T* pw = ptw + (size_t)p * kPtStride;
+          T u0 = pw[6] + pw[9] * df, u1 = pw[7] + pw[10] * df, u2 = pw[8] + pw[11] * df;
+          for (int k = ptr[p]; k < ptr[p + 1]; ++k) {
+            const int s = sm.slot[obs_cam(obs, k)];
+            if (s < 0) continue;
+            const T* Y = Ybuf + (size_t)k * kYStride;
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+              const T d = T(sm.dc[6 * s + r]);
+              u0 += Y[r * 3 + 0] * d;
+              u1 += Y[r * 3 + 1] * d;
+              u2 += Y[r * 3 + 2] * d;
+            }
+          }
+          const T L00 = pw[0], L10 = pw[1], L11 = pw[2], L20 = pw[3], L21 = pw[4], L22 = pw[5];
+          T x2 = u2 / L22;
+          T x1 = (u1 - L21 * x2) / L11;
+          T x0 = (u0 - L10 * x1 - L20 * x2) / L00;
+          pw[12] = -x0;
+          pw[13] = -x1;
+          pw[14] = -x2;
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---------- K5 trials, accept / reject, lambda (miniba.py:244-293) ----------
+    if (tid == 0) lambdas[it] = lam;
+    int tries = 0, took = -1;
+    double tc_[3] = {0, 0, 0};
+    double ft = f;
+    if (!chol_fail) {
+      for (int bt = 0; bt < kBacktrackTries; ++bt) {
+        const double frac = ldexp(1.0, -bt);
+        for (int c = tid; c < n; c += blockDim.x) {
+          const int s = sm.slot[c];
+          if (s < 0) {
+            for (int i = 0; i < 9; ++i) sm.Rt[9 * c + i] = sm.Rc[9 * c + i];
+            for (int i = 0; i < 3; ++i) sm.tt[3 * c + i] = sm.tc[3 * c + i];
+          } else {
+            double w[3] = {frac * sm.dc[6 * s], frac * sm.dc[6 * s + 1], frac * sm.dc[6 * s + 2]};
+            double E[9];
+            exp_so3(w, E);
+            matmul33(E, sm.Rc + 9 * c, sm.Rt + 9 * c);
+            for (int i = 0; i < 3; ++i) sm.tt[3 * c + i] = sm.tc[3 * c + i] + frac * sm.dc[6 * s + 3 + i];
+          }
+        }
+        ft = has_f ? f + frac * sm.dc[FI] : f;
+        __syncthreads();
+        cost_pass<T>(obs, lo, K, X, ptw, frac, opt_pts, sm.Rt, sm.tt, ft, cx, cy, delta, loss,
+                     sm.red, tc_);
+        ++tries;
+        if (tc_[0] < cost && isfinite(tc_[0])) {
+          took = bt;
+          break;
+        }
+      }
+    }
+    if (tid == 0) evals[it] = (uint8_t)tries;
+    bool stop = false;
+    if (took >= 0) {
+      const double frac = ldexp(1.0, -took);
+      for (int i = tid; i < n * 9; i += blockDim.x) sm.Rc[i] = sm.Rt[i];
+      for (int i = tid; i < n * 3; i += blockDim.x) sm.tc[i] = sm.tt[i];
+      if (opt_pts)
+        for (int p = tid; p < Pn; p += blockDim.x) {
+          const T* dp = ptw + (size_t)p * kPtStride + 12;
+          X[3 * p + 0] = X[3 * p + 0] + frac * (double)dp[0];
+          X[3 * p + 1] = X[3 * p + 1] + frac * (double)dp[1];
+          X[3 * p + 2] = X[3 * p + 2] + frac * (double)dp[2];
+        }
+      f = ft;
+      lam = took == 0 ? fmax(lam / nu, 1e-15) : fmin(lam * nu, kLambdaMax);
+      const double improve = cost - tc_[0];
+      cost = tc_[0];
+      se = tc_[1];
+      se2 = tc_[2];
+      if (tid == 0) accepted[it] = 1;
+      if (improve <= 1e-15 * fmax(cost, 1.0)) {
+        stop = true;
+        stop_reason = MBA_SOLVE_CONVERGED;
+      }
+    } else {
+      lam = fmin(lam * nu, kLambdaMax);
+      if (tid == 0) accepted[it] = 0;
+      if (!chol_fail && lam >= kLambdaMax) {
+        stop = true;
+        stop_reason = MBA_SOLVE_LAMBDA_CAP;
+      }
+    }
+    if (tid == 0) costs[it + 1] = cost;
+    ++it;
+    __syncthreads();
+    if (stop) break;
+  }
+
+  // ---------------- outputs ----------------
+  for (int i = tid; i < n * 9; i += blockDim.x) O.R_out[cb * 9 + i] = sm.Rc[i];
+  for (int i = tid; i < n * 3; i += blockDim.x) O.t_out[cb * 3 + i] = sm.tc[i];
+  if (tid == 0) {
+    O.focal_out[b] = f;
+    O.n_iters[b] = it;
+    O.status[b] = stop_reason;
+    O.final_stats[4 * b + 0] = cost;
+    O.final_stats[4 * b + 1] = se;
+    O.final_stats[4 * b + 2] = se2;
+    O.final_stats[4 * b + 3] = (double)K;
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) solve_kernel(SolveParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_prob;
+  for (;;) {
+    if (threadIdx.x == 0) s_prob = atomicAdd(P.counter, 1);
+    __syncthreads();
+    const int b = s_prob;
+    __syncthreads();
+    if (b >= P.d.n_problems) return;
+    solve_one<T>(P, b, smem_raw);
+  }
+}
+
+template <typename T>
+static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
+                  size_t ws_bytes, cudaStream_t st) {
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = smem_bytes<T>(d->max_cams);
+  if (smem > 200 * 1024) return MBA_ERR_TOO_LARGE;
+  cudaFuncSetAttribute(solve_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<T>, kThreads, smem);
+  if (per_sm < 1) return MBA_ERR_TOO_LARGE;
+  int grid = n_sm * per_sm;
+  if (grid > d->n_problems) grid = d->n_problems;
+  const size_t slot = ws_slot_bytes<T>(d->max_obs, d->max_points);
+  if (ws_bytes < 256 + slot * (size_t)grid) return MBA_ERR_INVALID;
+  SolveParams P;
+  P.d = *d;
+  P.cfg = *cfg;
+  P.o = *o;
+  P.counter = (int*)ws;
+  P.ws = (unsigned char*)ws + 256;
+  P.ws_slot_bytes = slot;
+  P.max_cams = d->max_cams;
+  cudaMemsetAsync(ws, 0, sizeof(int), st);
+  solve_kernel<T><<<grid, kThreads, smem, st>>>(P);
+  return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
+}
+
+}  // namespace mba
+
+extern "C" {
+
+int32_t mba_abi_version(void) { return MBA_ABI_VERSION; }
+
+size_t mba_workspace_bytes(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n_sm = 148;
+  const bool f64 = cfg->precision == MBA_LIN_F64;
+  const size_t slot = f64 ? mba::ws_slot_bytes<double>(d->max_obs, d->max_points)
+                          : mba::ws_slot_bytes<float>(d->max_obs, d->max_points);
+  size_t grid = (size_t)n_sm * 8;  // upper bound on resident CTAs
+  if (grid > (size_t)d->n_problems) grid = d->n_problems;
+  return 256 + slot * grid;
+}
+
+int32_t mba_solve(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o,
+                  void* ws, size_t ws_bytes, void* stream) {
+  if (!d || !cfg || !o || d->n_problems < 0 || cfg->max_iters < 0) return MBA_ERR_INVALID;
+  if (d->n_problems == 0) return MBA_OK;
+  if (d->max_cams < 1 || d->max_obs < 1) return MBA_ERR_EMPTY;
+  if (d->max_obs > 0x7fffffff || d->max_points > 0x7ffffffe) return MBA_ERR_TOO_LARGE;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cfg->precision == MBA_LIN_F64) return mba::launch<double>(d, cfg, o, ws, ws_bytes, st);
+  return mba::launch<float>(d, cfg, o, ws, ws_bytes, st);
+}
+
+}  // extern "C"

@@ -21,7 +21,12 @@ from dataclasses import dataclass
 import numpy as np
 
 WIDTH, HEIGHT, F_TRUE = 640, 480, 520.0
-CHUNK = 256                      # problems per RNG stream
+CHUNK = 256                      # problems per RNG stream (at most)
+
+
+def chunk_size(K):
+    """Problems per RNG stream: up to 256, about 1M observations per chunk."""
+    return int(min(CHUNK, max(1, (1 << 20) // max(int(K), 1))))
 
 
 @dataclass
@@ -146,13 +151,30 @@ def _chunk(rng, nb, n, K, noise_px, outlier_frac):
                 uv=uv, K=np.bincount(ob, minlength=nb))
 
 
-def make_batch(n_problems, n_cams=8, K=2000, seed=0, noise_px=0.5, outlier_frac=0.0):
-    """Generate `n_problems` independent problems."""
-    parts = []
-    for c0 in range(0, n_problems, CHUNK):
-        nb = min(CHUNK, n_problems - c0)
-        rng = np.random.default_rng(np.random.SeedSequence([int(seed), 0xBA8D, c0 // CHUNK]))
-        parts.append(_chunk(rng, nb, n_cams, K, noise_px, outlier_frac))
+def _chunk_job(args):
+    seed, ci, nb, n_cams, K, noise_px, outlier_frac = args
+    rng = np.random.default_rng(np.random.SeedSequence([int(seed), 0xBA8D, ci]))
+    return _chunk(rng, nb, n_cams, K, noise_px, outlier_frac)
+
+
+def make_batch(n_problems, n_cams=8, K=2000, seed=0, noise_px=0.5, outlier_frac=0.0, first=0,
+               workers=1):
+    """Generate problems [first, first + n_problems) of the seeded stream
+    (SURVEY 8d). Problem i depends only on (seed, i), so any contiguous shard
+    can be generated independently. `workers` > 1 generates chunks in
+    parallel processes."""
+    ch = chunk_size(K)
+    c_lo, c_hi = first // ch, (first + n_problems + ch - 1) // ch
+    jobs = [(seed, ci, ch, n_cams, K, noise_px, outlier_frac) for ci in range(c_lo, c_hi)]
+    if workers > 1 and len(jobs) > 1:
+        from concurrent.futures import ProcessPoolExecutor
+        with ProcessPoolExecutor(max_workers=min(workers, len(jobs))) as ex:
+            parts = list(ex.map(_chunk_job, jobs))
+    else:
+        parts = [_chunk_job(j) for j in jobs]
+    lo = first - c_lo * ch
+    if lo or (c_hi - c_lo) * ch != n_problems:
+        parts = _slice_parts(parts, lo, n_problems)
     cat = lambda k: np.concatenate([p[k] for p in parts])
     P = cat("P")
     Kb = cat("K")
@@ -169,6 +191,30 @@ def make_batch(n_problems, n_cams=8, K=2000, seed=0, noise_px=0.5, outlier_frac=
         cam=cat("cam"), pt=cat("pt"), uv=_f32(cat("uv")), fixed=fixed.reshape(-1),
         gt_R=cat("R").reshape(-1, 3, 3), gt_t=cat("t").reshape(-1, 3),
         gt_points=cat("Xg"))
+
+
+def _slice_parts(parts, lo, count):
+    """Keep problems [lo, lo + count) of the concatenated chunk list."""
+    keys_b = ("R", "t", "R0", "t0")          # (nb, n, ...)
+    out = []
+    base = 0
+    for p in parts:
+        nb = len(p["P"])
+        a, b = max(lo - base, 0), min(lo + count - base, nb)
+        base += nb
+        if a >= b:
+            continue
+        P, Kb = p["P"], p["K"]
+        p_first = np.concatenate([[0], np.cumsum(P)])
+        o_first = np.concatenate([[0], np.cumsum(Kb)])
+        q = {k: p[k][a:b] for k in keys_b}
+        q["P"], q["K"] = P[a:b], Kb[a:b]
+        for k in ("Xg", "X0"):
+            q[k] = p[k][p_first[a]:p_first[b]]
+        for k in ("cam", "pt", "uv"):
+            q[k] = p[k][o_first[a]:o_first[b]]
+        out.append(q)
+    return out
 
 
 # BASELINE.json configs (SURVEY 8d table)

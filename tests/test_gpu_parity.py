@@ -1,0 +1,111 @@
+"""Device parity: the sm_100a solver against the reference's golden outputs
+and against the CPU oracle on seeded synthetic problems (SURVEY.md 8c rule:
+accept/reject, backtrack counts and lambda identical through the plateau
+index i*; final cost rel <= 1e-4, rotation <= 1e-4 rad, translation rel <= 1e-4)."""
+import numpy as np
+import pytest
+
+from conftest import golden_cases, golden_ids, load_case
+from gpu_helpers import assert_parity, rot_err, run_device
+from oracle import miniba_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("precision", ["mixed", "f64"])
+@pytest.mark.parametrize("path", golden_cases(), ids=golden_ids())
+def test_solver_matches_reference_golden(path, precision, cuda_ok):
+    prob, cfg, out = load_case(path)
+    dev = run_device([prob], cfg, precision)[0]
+    assert_parity(dev, out["costs"], out["accepted"], out["evals"], out["lambdas"], out["R"],
+                  out["t"], float(out["focal"]), label=f"{path}:{precision}")
+
+
+@pytest.mark.parametrize("precision", ["mixed", "f64"])
+def test_batched_matches_oracle_and_is_shard_invariant(precision, cuda_ok):
+    from paper_2506_05558_b200.synth import make_batch
+    b = make_batch(12, n_cams=8, K=2000, seed=3)
+    probs = [b.problem(i) for i in range(12)]
+    cfg = dict(max_iters=200)
+    dev_all = run_device(probs, cfg, precision)
+    dev_a = run_device(probs[:5], cfg, precision)
+    dev_b = run_device(probs[5:], cfg, precision)
+    for i, d in enumerate(dev_all):
+        other = dev_a[i] if i < 5 else dev_b[i - 5]
+        # bit-identical regardless of how the batch is sharded
+        np.testing.assert_array_equal(d["costs"], other["costs"])
+        np.testing.assert_array_equal(d["points"], other["points"])
+        np.testing.assert_array_equal(d["R"], other["R"])
+    for i in range(0, 12, 3):
+        p = b.problem(i)
+        ref = O.lm(p, max_iters=200)
+        assert_parity(dev_all[i], ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"],
+                      p["R"], p["t"], p["focal"], label=f"batch[{i}]")
+
+
+def test_deterministic_repeat(cuda_ok):
+    from paper_2506_05558_b200.synth import make_batch
+    b = make_batch(4, n_cams=8, K=2000, seed=9)
+    probs = [b.problem(i) for i in range(4)]
+    a = run_device(probs, dict(max_iters=50))
+    c = run_device(probs, dict(max_iters=50))
+    for x, y in zip(a, c):
+        np.testing.assert_array_equal(x["costs"], y["costs"])
+        np.testing.assert_array_equal(x["points"], y["points"])
+
+
+@pytest.mark.parametrize("precision", ["mixed", "f64"])
+def test_paper_scale_single_problem(precision, cuda_ok):
+    """BASELINE config 2: 8 frames, K = 20k, Huber."""
+    from paper_2506_05558_b200.synth import make_batch
+    p = make_batch(1, n_cams=8, K=20000, seed=2).problem(0)
+    dev = run_device([p], dict(max_iters=200), precision)[0]
+    ref = O.lm(p, max_iters=200)
+    assert_parity(dev, ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"], p["R"], p["t"],
+                  p["focal"], label="cfg2")
+
+
+def test_cauchy_outliers_many_cameras(cuda_ok):
+    """Config-5 shape at oracle-friendly size: 16 frames, 20% outliers, Cauchy
+    (extension; parity against the oracle only -- unpinned by the reference)."""
+    from paper_2506_05558_b200.synth import make_batch
+    p = make_batch(1, n_cams=16, K=6000, seed=5, outlier_frac=0.2).problem(0)
+    dev = run_device([p], dict(max_iters=30, loss="cauchy"), "f64")[0]
+    ref = O.lm(p, max_iters=30, loss="cauchy")
+    assert_parity(dev, ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"], p["R"], p["t"],
+                  p["focal"], label="cauchy16")
+
+
+def test_fault_injection_matches_oracle(cuda_ok):
+    from paper_2506_05558_b200.synth import make_batch
+    p = make_batch(1, n_cams=8, K=2000, seed=4).problem(0)
+    fail = (0, 1, 4)
+    dev = run_device([p], dict(max_iters=200, fail_at=fail), "f64")[0]
+    ref = O.lm(p, max_iters=200, fail_at=fail)
+    for i in fail:
+        assert not dev["accepted"][i] and dev["evals"][i] == 0
+    assert_parity(dev, ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"], p["R"], p["t"],
+                  p["focal"], label="fault")
+
+
+def test_max_iters_zero_and_one(cuda_ok):
+    from paper_2506_05558_b200.synth import make_batch
+    p = make_batch(1, n_cams=5, K=600, seed=8).problem(0)
+    d0 = run_device([p], dict(max_iters=0))[0]
+    assert len(d0["costs"]) == 1 and len(d0["accepted"]) == 0
+    np.testing.assert_array_equal(d0["points"], p["points"])
+    ref = O.lm(dict(p), max_iters=1)
+    d1 = run_device([p], dict(max_iters=1), "f64")[0]
+    assert d1["accepted"].tolist() == ref["accepted"].tolist()
+    np.testing.assert_allclose(d1["costs"], ref["costs"], rtol=1e-9)
+
+
+def test_all_cameras_fixed_focal_only(cuda_ok):
+    """C = 1 (focal only) and C = 0 edge shapes."""
+    from paper_2506_05558_b200.synth import make_batch
+    p = make_batch(1, n_cams=4, K=500, seed=6).problem(0)
+    p["fixed_cams"] = np.ones(4, dtype=bool)
+    dev = run_device([p], dict(max_iters=40), "f64")[0]
+    ref = O.lm(dict(p), max_iters=40)
+    np.testing.assert_allclose(dev["costs"][-1], ref["costs"][-1], rtol=1e-6)
+    assert dev["accepted"][:3].tolist() == ref["accepted"][:3].tolist()
