@@ -192,7 +192,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--problems", type=int, default=None, help="override the problem count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="mixed", choices=["mixed", "f64"])
+    ap.add_argument("--precision", default="f64", choices=["mixed", "f64"])
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -66,6 +66,8 @@ typedef struct {
   int32_t max_cams;          /* max cameras in any problem            */
   int64_t max_obs;           /* max observations in any problem       */
   int64_t max_points;        /* max points in any problem             */
+  int64_t max_pairs;         /* max over problems of sum_p m_p (m_p + 1) / 2, m_p =
+                                observations of point p (co-observation pairs)  */
   const int64_t* cam_off;    /* camera rows of problem b: [cam_off[b], cam_off[b+1]) */
   const int64_t* pt_off;
   const int64_t* obs_off;

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libminiba.so")
+LIB_PATH = os.environ.get("MBA_LIB", os.path.join(HERE, "libminiba.so"))
 
 MBA_OK, MBA_ERR_INVALID, MBA_ERR_TOO_LARGE, MBA_ERR_CUDA, MBA_ERR_EMPTY, MBA_ERR_NOT_PD = 0, -1, -2, -3, -4, -5
 LOSS = {"huber": 0, "cauchy": 1}
@@ -23,7 +23,7 @@ _vp = ct.c_void_p
 
 class MbaBatchDesc(ct.Structure):
     _fields_ = [("n_problems", ct.c_int32), ("max_cams", ct.c_int32), ("max_obs", ct.c_int64),
-                ("max_points", ct.c_int64), ("cam_off", _vp), ("pt_off", _vp), ("obs_off", _vp),
+                ("max_points", ct.c_int64), ("max_pairs", ct.c_int64), ("cam_off", _vp), ("pt_off", _vp), ("obs_off", _vp),
                 ("obs", _vp), ("obs_lo", _vp), ("fixed", _vp), ("cx", _vp), ("cy", _vp),
                 ("flags", _vp)]
 

@@ -5,29 +5,35 @@
 // solve_step(method="schur") (180-220).
 //
 // Execution model: a persistent grid; each CTA pulls whole problems from an
-// atomic work counter and runs the complete LM loop for that problem on chip:
+// atomic work counter and runs the complete LM loop for that problem on chip.
 //
-//   setup      point CSR (binary search), camera-major permutation (warp ballots)
-//   cost pass  one thread per observation, 16-byte record loads, fp64 residual
-//              and robust cost, deterministic block reduction
-//   per iteration:
-//     K1+K2  point pass    one thread per point: fp64 residuals, Jacobians in
-//                          T (float or double), V_p / g_p / W_i accumulation in
-//                          registers, 3x3 Cholesky of the damped V_p, and the
-//                          Schur factors Y_i = W_i L_p^-T, z_p, y_f (K3 prep)
-//     K2     camera jobs   one warp per free camera: U_cc, U_cf, g_c
-//     K3     pair jobs     one warp per camera pair (a<=b): S_ab -= sum Y_i Y_j^T
-//                          (all reductions are fixed-order warp butterflies;
-//                          no atomics, bit-reproducible)
-//     K4     Cholesky      packed reduced camera system in shared memory,
-//                          forward/back substitution for dc
-//            back-sub      dp_p = -L_p^-T (z_p + sum Y_i^T dc + y_f df)
-//     K5     trials        <= 5 backtracking cost passes (fp64), accept/reject,
-//                          lambda schedule and termination -- all on device
+//   setup (once per solve)
+//     point CSR by binary search over the point-major observations, the
+//     camera-major permutation (warp ballots), and the co-observation pair
+//     lists: for every free camera block (a <= b) the list of observation
+//     pairs (i in a, j in b, same point). Built once, they turn the Schur
+//     accumulation into a divergence-free stream.
+//   cost pass   one thread per observation, 16-byte record loads, fp64
+//               residual and robust cost, deterministic block reduction
+//   per iteration
+//     K1+K2 point pass   one thread per point: fp64 residual, Jacobians in T,
+//                        V_p / g_p accumulation in registers, W_i = w A^T B,
+//                        damped 3x3 Cholesky V_p = L L^T and the Schur factors
+//                        Y_i = W_i L^-T, z_p = L^-1 g_p, y_f = L^-1 Wf_p
+//     K2 camera jobs     one warp per free camera: U_aa, U_af, g_a and the
+//                        Schur focal column / rhs terms sum Y_i y_f, sum Y_i z
+//     K3 pair jobs       one warp per camera block: S_ab = -sum Y_i Y_j^T over
+//                        the block's pair list (fixed-order warp butterflies:
+//                        no atomics, bit-reproducible)
+//     K4 LDL^T           packed reduced camera system in shared memory, one
+//                        barrier per column, then forward/back substitution
+//        back-sub        dp_p = -L_p^-T (z_p + sum Y_i^T dc + y_f df)
+//     K5 trials          <= 5 backtracking cost passes (fp64), accept/reject,
+//                        lambda schedule and termination -- all on device
 //
 // State (cameras, focal, points) is float64; T selects the arithmetic of the
-// linearise/Schur/Cholesky stages (mixed-precision iterative refinement when
-// T = float, SURVEY 8c design (b)).
+// linearise/Schur/factorisation stages (float = mixed-precision iterative
+// refinement, SURVEY 8c design (b); double = full float64).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -38,9 +44,25 @@ namespace mba {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kPtStride = 16;   // per-point workspace: L(6) z(3) yf(3) dp(3) pad
-constexpr int kYStride = 18;    // per-observation workspace: W_i then Y_i (6x3)
-constexpr int kUcamStride = 33; // per free camera: U_aa lower(21) U_af(6) g_a(6)
+constexpr int kPtStride = 16;    // per point: L(6) z(3) yf(3) dp(3) pad
+constexpr int kYStride = 20;     // per observation: W_i then Y_i (6x3), padded for 16B vectors
+constexpr int kUcamStride = 45;  // per free camera: U_aa lower(21) U_af(6) g_a(6) Sy_f(6) Sy_z(6)
+
+// Optional per-phase cycle counters (build with -DMBA_PHASE_PROF; see
+// paper_2506_05558_b200/build.py --prof). Thread 0 of every CTA accumulates
+// clock64() deltas between phase boundaries; totals land in g_prof[phase].
+enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_N };
+#ifdef MBA_PHASE_PROF
+__device__ unsigned long long* g_prof = nullptr;
+#define PROF_DECL __shared__ long long s_prof[PH_N]; long long prof_t = clock64(); \
+  if (threadIdx.x == 0) for (int i = 0; i < PH_N; ++i) s_prof[i] = 0;
+#define PROF_MARK(ph) if (threadIdx.x == 0) { long long now = clock64(); s_prof[ph] += now - prof_t; prof_t = now; }
+#define PROF_FLUSH if (threadIdx.x == 0 && g_prof) for (int i = 0; i < PH_N; ++i) atomicAdd(g_prof + i, (unsigned long long)s_prof[i]);
+#else
+#define PROF_DECL
+#define PROF_MARK(ph)
+#define PROF_FLUSH
+#endif
 
 struct SolveParams {
   MbaBatchDesc d;
@@ -62,18 +84,20 @@ struct Smem {
   double* red;  // [kWarps * 4]
   T* S;         // packed lower [Cmax(Cmax+1)/2]
   T* rhs;       // [Cmax]
-  T* ucam;      // [nfmax * 33]
-  T* pairf;     // [nfmax * 12]
+  T* ucam;      // [nfmax * kUcamStride]
   int* cam_ptr; // [n+1]
   int* slot;    // [n]
   int* cam_of_slot;  // [n]
+  int* blk_off;      // [nbmax+1] pair-list offsets per camera block
+  unsigned char* blk_a;  // [nbmax] block -> (slot a, slot b)
+  unsigned char* blk_b;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 template <typename T>
 __host__ __device__ inline size_t smem_bytes(int max_cams) {
-  size_t n = max_cams, C = 6 * n + 1;
+  size_t n = max_cams, C = 6 * n + 1, nb = n * (n + 1) / 2;
   size_t b = 0;
   b += align16(sizeof(double) * n * 24);
   b += align16(sizeof(double) * C);
@@ -81,16 +105,17 @@ __host__ __device__ inline size_t smem_bytes(int max_cams) {
   b += align16(sizeof(T) * C * (C + 1) / 2);
   b += align16(sizeof(T) * C);
   b += align16(sizeof(T) * n * kUcamStride);
-  b += align16(sizeof(T) * n * 12);
   b += align16(sizeof(int) * (n + 1));
   b += align16(sizeof(int) * n * 2);
+  b += align16(sizeof(int) * (nb + 1));
+  b += align16(2 * nb);
   return b;
 }
 
 template <typename T>
 __device__ inline Smem<T> carve(unsigned char* base, int max_cams) {
   Smem<T> s;
-  size_t n = max_cams, C = 6 * n + 1, off = 0;
+  size_t n = max_cams, C = 6 * n + 1, nb = n * (n + 1) / 2, off = 0;
   auto take = [&](size_t bytes) { unsigned char* p = base + off; off += align16(bytes); return p; };
   double* cams = (double*)take(sizeof(double) * n * 24);
   s.Rc = cams;
@@ -102,22 +127,59 @@ __device__ inline Smem<T> carve(unsigned char* base, int max_cams) {
   s.S = (T*)take(sizeof(T) * C * (C + 1) / 2);
   s.rhs = (T*)take(sizeof(T) * C);
   s.ucam = (T*)take(sizeof(T) * n * kUcamStride);
-  s.pairf = (T*)take(sizeof(T) * n * 12);
   s.cam_ptr = (int*)take(sizeof(int) * (n + 1));
   int* sl = (int*)take(sizeof(int) * n * 2);
   s.slot = sl;
   s.cam_of_slot = sl + n;
+  s.blk_off = (int*)take(sizeof(int) * (nb + 1));
+  s.blk_a = (unsigned char*)take(2 * nb);
+  s.blk_b = s.blk_a + nb;
   return s;
 }
 
 template <typename T>
-__host__ __device__ inline size_t ws_slot_bytes(int64_t max_obs, int64_t max_points) {
+__host__ __device__ inline size_t ws_slot_bytes(int64_t max_obs, int64_t max_points, int64_t max_pairs) {
   size_t b = 0;
   b += align16(sizeof(int) * max_obs);              // camera-major permutation
   b += align16(sizeof(int) * (max_points + 1));     // point CSR
+  b += align16(sizeof(int2) * max_pairs);           // pair lists
   b += align16(sizeof(T) * kYStride * max_obs);     // W_i / Y_i
   b += align16(sizeof(T) * kPtStride * max_points); // per-point factors
   return b;
+}
+
+// ---- vector helpers for the 18-value Y blocks ------------------------------
+
+__device__ __forceinline__ void load18(const float* p, float y[18]) {
+  const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float4 v = q[i];
+    y[4 * i] = v.x; y[4 * i + 1] = v.y; y[4 * i + 2] = v.z; y[4 * i + 3] = v.w;
+  }
+  float2 v = reinterpret_cast<const float2*>(p)[8];
+  y[16] = v.x;
+  y[17] = v.y;
+}
+__device__ __forceinline__ void store18(float* p, const float y[18]) {
+  float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) q[i] = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+  reinterpret_cast<float2*>(p)[8] = make_float2(y[16], y[17]);
+}
+__device__ __forceinline__ void load18(const double* p, double y[18]) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    double2 v = q[i];
+    y[2 * i] = v.x;
+    y[2 * i + 1] = v.y;
+  }
+}
+__device__ __forceinline__ void store18(double* p, const double y[18]) {
+  double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) q[i] = make_double2(y[2 * i], y[2 * i + 1]);
 }
 
 struct Obs {
@@ -145,28 +207,59 @@ __device__ __forceinline__ int obs_cam(const MbaObs* __restrict__ obs, int64_t k
   return __ldg(&obs[k].cam);
 }
 
+__device__ __forceinline__ int warp_excl_scan(int v, int lane) {
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x - v;
+}
+
 // Cost pass over all observations with camera set (Rs, ts, f) and points
-// X + frac * dp. Returns (sum rho, sum e, sum e^2) to every thread.
+// X + frac * dp. Four observations per thread are in flight at once.
+// Returns (sum rho, sum e, sum e^2) to every thread.
 template <typename T>
 __device__ void cost_pass(const MbaObs* __restrict__ obs, const float* __restrict__ lo, int K,
                           const double* __restrict__ X, const T* __restrict__ ptw, double frac,
                           bool use_dp, const double* Rs, const double* ts, double f, double cx,
                           double cy, double delta, int loss, double* red, double out[3]) {
+  constexpr int U = 4;
   double acc[3] = {0.0, 0.0, 0.0};
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    Obs o = load_obs(obs, lo, k);
-    double Xp[3] = {X[3 * o.pt + 0], X[3 * o.pt + 1], X[3 * o.pt + 2]};
-    if (use_dp) {
-      const T* dp = ptw + (size_t)o.pt * kPtStride + 12;
-      Xp[0] = Xp[0] + frac * (double)dp[0];
-      Xp[1] = Xp[1] + frac * (double)dp[1];
-      Xp[2] = Xp[2] + frac * (double)dp[2];
+  for (int k0 = threadIdx.x; k0 < K; k0 += U * blockDim.x) {
+    Obs o[U];
+    double Xp[U][3];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * blockDim.x;
+      if (k < K) o[u] = load_obs(obs, lo, k);
     }
-    Proj pr = project_residual(Rs + 9 * o.cam, ts + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
-    double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
-    acc[0] += robust_rho(e, delta, loss);
-    acc[1] += e;
-    acc[2] += e * e;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * blockDim.x;
+      if (k >= K) continue;
+      const double* x = X + 3 * o[u].pt;
+      Xp[u][0] = x[0];
+      Xp[u][1] = x[1];
+      Xp[u][2] = x[2];
+      if (use_dp) {
+        const T* dp = ptw + (size_t)o[u].pt * kPtStride + 12;
+        Xp[u][0] = Xp[u][0] + frac * (double)dp[0];
+        Xp[u][1] = Xp[u][1] + frac * (double)dp[1];
+        Xp[u][2] = Xp[u][2] + frac * (double)dp[2];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * blockDim.x;
+      if (k >= K) continue;
+      Proj pr = project_residual_fast(Rs + 9 * o[u].cam, ts + 3 * o[u].cam, Xp[u], f, cx, cy, o[u].u, o[u].v);
+      double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
+      acc[0] += robust_rho(e, delta, loss);
+      acc[1] += e;
+      acc[2] += e * e;
+    }
   }
   block_sum<double, 3>(acc, red);
   out[0] = acc[0];
@@ -181,7 +274,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   const MbaLmConfig& cfg = P.cfg;
   const MbaOutputs& O = P.o;
   Smem<T> sm = carve<T>(smem_raw, P.max_cams);
-  __shared__ int s_flag;        // setup error / Cholesky failure
+  __shared__ int s_flag;        // setup error
   __shared__ int s_C, s_nf;
   __shared__ double s_red4[kWarps * 4];
 
@@ -201,7 +294,8 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   unsigned char* ws = P.ws + (size_t)blockIdx.x * P.ws_slot_bytes;
   int* perm = (int*)ws;
   int* ptr = (int*)(ws + align16(sizeof(int) * D.max_obs));
-  T* Ybuf = (T*)((unsigned char*)ptr + align16(sizeof(int) * (D.max_points + 1)));
+  int2* pairs = (int2*)((unsigned char*)ptr + align16(sizeof(int) * (D.max_points + 1)));
+  T* Ybuf = (T*)((unsigned char*)pairs + align16(sizeof(int2) * D.max_pairs));
   T* ptw = (T*)((unsigned char*)Ybuf + align16(sizeof(T) * kYStride * D.max_obs));
 
   double* costs = O.costs + (size_t)b * (max_it + 1);
@@ -209,6 +303,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   uint8_t* accepted = O.accepted + (size_t)b * max_it;
   uint8_t* evals = O.evals + (size_t)b * max_it;
 
+  PROF_DECL
   // ---------------- setup ----------------
   for (int i = tid; i < n * 9; i += blockDim.x) sm.Rc[i] = O.R_in[cb * 9 + i];
   for (int i = tid; i < n * 3; i += blockDim.x) sm.tc[i] = O.t_in[cb * 3 + i];
@@ -225,11 +320,17 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
         ++nf;
       }
     }
+    int q = 0;
+    for (int a = 0; a < nf; ++a)
+      for (int bb = a; bb < nf; ++bb, ++q) {
+        sm.blk_a[q] = (unsigned char)a;
+        sm.blk_b[q] = (unsigned char)bb;
+      }
     s_nf = nf;
     s_C = 6 * nf + (has_f ? 1 : 0);
     s_flag = 0;
   }
-  // point CSR: obs are point-major; ptr[p] = first k with pt >= p
+  // point CSR: observations are point-major; ptr[p] = first k with pt >= p
   for (int p = tid; p <= Pn; p += blockDim.x) {
     int lo_i = 0, hi_i = K;
     while (lo_i < hi_i) {
@@ -238,7 +339,6 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     }
     ptr[p] = lo_i;
   }
-  // validate ordering and index ranges
   for (int k = tid; k < K; k += blockDim.x) {
     int pt = __ldg(&obs[k].pt), c = __ldg(&obs[k].cam);
     bool bad = pt < 0 || pt >= Pn || c < 0 || c >= n || (k > 0 && __ldg(&obs[k - 1].pt) > pt);
@@ -271,7 +371,41 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       base += __popc(m);
     }
   }
+  __syncthreads();
   const int nf = s_nf, C = s_C, FI = C - 1;
+  const int nb = opt_pts ? nf * (nf + 1) / 2 : 0;
+  // co-observation pair lists per camera block (a <= b): count, scan, fill
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int blk = wid; blk < nb; blk += kWarps) {
+      const int ca = sm.cam_of_slot[sm.blk_a[blk]], cbb = sm.cam_of_slot[sm.blk_b[blk]];
+      const int q1 = sm.cam_ptr[ca + 1];
+      int base = pass ? sm.blk_off[blk] : 0;
+      for (int q0 = sm.cam_ptr[ca]; q0 < q1; q0 += 32) {
+        const int q = q0 + lane;
+        int i = -1, j0 = 0, j1 = 0, m = 0;
+        if (q < q1) {
+          i = perm[q];
+          const int pt = __ldg(&obs[i].pt);
+          j0 = ptr[pt];
+          j1 = ptr[pt + 1];
+          for (int j = j0; j < j1; ++j) m += obs_cam(obs, j) == cbb;
+        }
+        if (pass) {
+          int pos = base + warp_excl_scan(m, lane);
+          for (int j = j0; j < j1 && m; ++j)
+            if (obs_cam(obs, j) == cbb) pairs[pos++] = make_int2(i, j);
+        }
+        base += warp_sum(m);
+      }
+      if (!pass && lane == 0) sm.blk_off[blk + 1] = base;
+    }
+    __syncthreads();
+    if (!pass && tid == 0) {
+      sm.blk_off[0] = 0;
+      for (int q = 0; q < nb; ++q) sm.blk_off[q + 1] += sm.blk_off[q];
+    }
+    __syncthreads();
+  }
   double f = O.focal_in[b];
   if (s_flag) {  // malformed problem: report and leave parameters untouched
     if (tid == 0) {
@@ -284,11 +418,12 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     __syncthreads();
     return;
   }
-  __syncthreads();
 
+  PROF_MARK(PH_SETUP)
   // initial cost (miniba.py:232-235)
   double st[3];
   cost_pass<T>(obs, lo, K, X, ptw, 0.0, false, sm.Rc, sm.tc, f, cx, cy, delta, loss, sm.red, st);
+  PROF_MARK(PH_COST0)
   double cost = st[0], se = st[1], se2 = st[2];
   double lam = cfg.lambda_init;
   if (tid == 0) costs[0] = cost;
@@ -306,7 +441,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       for (int k = k0; k < k1; ++k) {
         Obs o = load_obs(obs, lo, k);
         const double* Rk = sm.Rc + 9 * o.cam;
-        Proj pr = project_residual(Rk, sm.tc + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
+        Proj pr = project_residual_fast(Rk, sm.tc + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
         double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
         T w = T(robust_w(e, delta, loss));
         T A[12], Fb[2], Bm[6];
@@ -334,11 +469,12 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
             for (int a = 0; a < 3; ++a) wf[a] += wf0 * Bm[a] + wf1 * Bm[3 + a];
           }
           if (sm.slot[o.cam] >= 0) {
-            T* Wk = Ybuf + (size_t)k * kYStride;
+            T W[18];
 #pragma unroll
             for (int r = 0; r < 6; ++r)
 #pragma unroll
-              for (int a = 0; a < 3; ++a) Wk[r * 3 + a] = A[r] * wB[a] + A[6 + r] * wB[3 + a];
+              for (int a = 0; a < 3; ++a) W[r * 3 + a] = A[r] * wB[a] + A[6 + r] * wB[3 + a];
+            store18(Ybuf + (size_t)k * kYStride, W);
           }
         }
       }
@@ -358,15 +494,18 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       for (int k = k0; k < k1; ++k) {
         if (sm.slot[obs_cam(obs, k)] < 0) continue;
         T* Wk = Ybuf + (size_t)k * kYStride;
+        T y[18];
+        load18(Wk, y);
 #pragma unroll
         for (int r = 0; r < 6; ++r) {
-          T y0 = Wk[r * 3 + 0] * i00;
-          T y1 = (Wk[r * 3 + 1] - L10 * y0) * i11;
-          T y2 = (Wk[r * 3 + 2] - L20 * y0 - L21 * y1) * i22;
-          Wk[r * 3 + 0] = y0;
-          Wk[r * 3 + 1] = y1;
-          Wk[r * 3 + 2] = y2;
+          T y0 = y[r * 3 + 0] * i00;
+          T y1 = (y[r * 3 + 1] - L10 * y0) * i11;
+          T y2 = (y[r * 3 + 2] - L20 * y0 - L21 * y1) * i22;
+          y[r * 3 + 0] = y0;
+          y[r * 3 + 1] = y1;
+          y[r * 3 + 2] = y2;
         }
+        store18(Wk, y);
       }
       T z0 = g[0] * i00, z1 = (g[1] - L10 * z0) * i11, z2 = (g[2] - L20 * z0 - L21 * z1) * i22;
       T f0 = wf[0] * i00, f1 = (wf[1] - L10 * f0) * i11, f2 = (wf[2] - L20 * f0 - L21 * f1) * i22;
@@ -378,22 +517,15 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       pw[9] = f0; pw[10] = f1; pw[11] = f2;
     }
     {
-      double pd[4] = {(double)part[0], (double)part[1], (double)part[2], (double)part[3]};
-      if (sizeof(T) == 4) {
-        // float partials are reduced in float to keep the arithmetic of T
-        T pf[4] = {part[0], part[1], part[2], part[3]};
-        block_sum<T, 4>(pf, (T*)s_red4);
-        for (int i = 0; i < 4; ++i) pd[i] = (double)pf[i];
-      } else {
-        block_sum<double, 4>(pd, s_red4);
-      }
-      part[0] = T(pd[0]); part[1] = T(pd[1]); part[2] = T(pd[2]); part[3] = T(pd[3]);
+      T pf[4] = {part[0], part[1], part[2], part[3]};
+      block_sum<T, 4>(pf, (T*)s_red4);
+      part[0] = pf[0]; part[1] = pf[1]; part[2] = pf[2]; part[3] = pf[3];
     }
     // (block_sum ended with __syncthreads: point factors are visible)
+    PROF_MARK(PH_POINT)
 
     // ---------- K2 camera jobs + K3 pair jobs (one warp per job) ----------
-    const int n_pair = opt_pts ? nf * (nf + 1) / 2 : 0;
-    for (int job = wid; job < nf + n_pair; job += kWarps) {
+    for (int job = wid; job < nf + nb; job += kWarps) {
       if (job < nf) {
         const int s = job, c = sm.cam_of_slot[s];
         const double* Rk = sm.Rc + 9 * c;
@@ -404,7 +536,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
           const int k = perm[q];
           Obs o = load_obs(obs, lo, k);
           const double Xp[3] = {X[3 * o.pt], X[3 * o.pt + 1], X[3 * o.pt + 2]};
-          Proj pr = project_residual(Rk, sm.tc + 3 * c, Xp, f, cx, cy, o.u, o.v);
+          Proj pr = project_residual_fast(Rk, sm.tc + 3 * c, Xp, f, cx, cy, o.u, o.v);
           double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
           T w = T(robust_w(e, delta, loss));
           T A[12], Fb[2], Bm[6];
@@ -419,73 +551,49 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
             acc[21 + r] += wa0 * Fb[0] + wa1 * Fb[1];
             acc[27 + r] += wa0 * r0 + wa1 * r1;
           }
+          if (opt_pts) {
+            T y[18];
+            load18(Ybuf + (size_t)k * kYStride, y);
+            const T* pw = ptw + (size_t)o.pt * kPtStride;
+            const T z0 = pw[6], z1 = pw[7], z2 = pw[8], f0 = pw[9], f1 = pw[10], f2 = pw[11];
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+              acc[33 + r] += y[r * 3] * f0 + y[r * 3 + 1] * f1 + y[r * 3 + 2] * f2;
+              acc[39 + r] += y[r * 3] * z0 + y[r * 3 + 1] * z1 + y[r * 3 + 2] * z2;
+            }
+          }
         }
 #pragma unroll
         for (int i = 0; i < kUcamStride; ++i) acc[i] = warp_sum(acc[i]);
         if (lane == 0)
           for (int i = 0; i < kUcamStride; ++i) sm.ucam[s * kUcamStride + i] = acc[i];
       } else {
-        // pair job index -> (sa <= sb)
-        int jj = job - nf, sa = 0;
-        while (jj >= nf - sa) { jj -= nf - sa; ++sa; }
-        const int sb = sa + jj;
-        const int ca = sm.cam_of_slot[sa], cbm = sm.cam_of_slot[sb];
-        const bool diag = sa == sb;
-        T acc[36], accf[6], accr[6];
+        const int blk = job - nf;
+        const int sa = sm.blk_a[blk], sb = sm.blk_b[blk];
+        T acc[36];
 #pragma unroll
         for (int i = 0; i < 36; ++i) acc[i] = T(0);
+        const int q1 = sm.blk_off[blk + 1];
+        for (int q = sm.blk_off[blk] + lane; q < q1; q += 32) {
+          const int2 pr = pairs[q];
+          T yi[18], yj[18];
+          load18(Ybuf + (size_t)pr.x * kYStride, yi);
+          load18(Ybuf + (size_t)pr.y * kYStride, yj);
 #pragma unroll
-        for (int i = 0; i < 6; ++i) accf[i] = accr[i] = T(0);
-        for (int q = sm.cam_ptr[ca] + lane; q < sm.cam_ptr[ca + 1]; q += 32) {
-          const int ki = perm[q];
-          const int pt = __ldg(&obs[ki].pt);
-          const T* Yi = Ybuf + (size_t)ki * kYStride;
-          T yi[18];
+          for (int r = 0; r < 6; ++r)
 #pragma unroll
-          for (int i = 0; i < 18; ++i) yi[i] = Yi[i];
-          const int j0 = ptr[pt], j1 = ptr[pt + 1];
-          for (int kj = j0; kj < j1; ++kj) {
-            if (obs_cam(obs, kj) != cbm) continue;
-            const T* Yj = Ybuf + (size_t)kj * kYStride;
-            T yj[18];
-#pragma unroll
-            for (int i = 0; i < 18; ++i) yj[i] = Yj[i];
-#pragma unroll
-            for (int r = 0; r < 6; ++r)
-#pragma unroll
-              for (int cc = 0; cc < 6; ++cc)
-                acc[r * 6 + cc] += yi[r * 3] * yj[cc * 3] + yi[r * 3 + 1] * yj[cc * 3 + 1] +
-                                   yi[r * 3 + 2] * yj[cc * 3 + 2];
-          }
-          if (diag) {
-            const T* pw = ptw + (size_t)pt * kPtStride;
-            T z0 = pw[6], z1 = pw[7], z2 = pw[8], f0 = pw[9], f1 = pw[10], f2 = pw[11];
-#pragma unroll
-            for (int r = 0; r < 6; ++r) {
-              accf[r] += yi[r * 3] * f0 + yi[r * 3 + 1] * f1 + yi[r * 3 + 2] * f2;
-              accr[r] += yi[r * 3] * z0 + yi[r * 3 + 1] * z1 + yi[r * 3 + 2] * z2;
-            }
-          }
+            for (int cc = 0; cc < 6; ++cc)
+              acc[r * 6 + cc] += yi[r * 3] * yj[cc * 3] + yi[r * 3 + 1] * yj[cc * 3 + 1] +
+                                 yi[r * 3 + 2] * yj[cc * 3 + 2];
         }
 #pragma unroll
         for (int i = 0; i < 36; ++i) acc[i] = warp_sum(acc[i]);
-        if (diag) {
-#pragma unroll
-          for (int i = 0; i < 6; ++i) {
-            accf[i] = warp_sum(accf[i]);
-            accr[i] = warp_sum(accr[i]);
-          }
-        }
         if (lane == 0) {
-          if (diag) {
+          if (sa == sb) {
             for (int r = 0; r < 6; ++r)
               for (int cc = 0; cc <= r; ++cc) sm.S[tri_idx(6 * sa + r, 6 * sa + cc)] = -acc[r * 6 + cc];
-            for (int i = 0; i < 6; ++i) {
-              sm.pairf[sa * 12 + i] = accf[i];
-              sm.pairf[sa * 12 + 6 + i] = accr[i];
-            }
           } else {
-            // block (sa, sb) with sa < sb lives at rows of sb in the lower triangle
+            // block (sa, sb), sa < sb, lives at rows of sb in the lower triangle
             for (int r = 0; r < 6; ++r)
               for (int cc = 0; cc < 6; ++cc) sm.S[tri_idx(6 * sb + r, 6 * sa + cc)] = -acc[cc * 6 + r];
           }
@@ -493,11 +601,11 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       }
     }
     __syncthreads();
+    PROF_MARK(PH_JOBS)
 
     // ---------- assemble damped S and rhs (miniba.py:188-213) ----------
     if (!opt_pts) {
       for (int i = tid; i < C * (C + 1) / 2; i += blockDim.x) sm.S[i] = T(0);
-      for (int i = tid; i < nf * 12; i += blockDim.x) sm.pairf[i] = T(0);
       __syncthreads();
     }
     for (int s = tid; s < nf; s += blockDim.x) {
@@ -509,11 +617,8 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
           if (r == cc) ud += tlam * (ud > T(kDiagFloor) ? ud : T(kDiagFloor));
           sm.S[tri_idx(6 * s + r, 6 * s + cc)] += ud;
         }
-        if (has_f) sm.S[tri_idx(FI, 6 * s + r)] = u[21 + r] - sm.pairf[s * 12 + r];
-        sm.rhs[6 * s + r] = -u[27 + r] + sm.pairf[s * 12 + 6 + r];
-      }
-      if (nf > 0 && s == 0) {
-        // off-diagonal camera blocks are pure Schur terms; zero them if points are fixed
+        if (has_f) sm.S[tri_idx(FI, 6 * s + r)] = u[21 + r] - (opt_pts ? u[33 + r] : T(0));
+        sm.rhs[6 * s + r] = -u[27 + r] + (opt_pts ? u[39 + r] : T(0));
       }
     }
     if (has_f && tid == 0) {
@@ -523,43 +628,39 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       sm.rhs[FI] = -part[1] + part[3];
     }
     __syncthreads();
+    PROF_MARK(PH_ASM)
 
-    // ---------- K4 Cholesky of the reduced camera system ----------
+    // ---------- K4 LDL^T of the reduced camera system, one barrier per column ----------
+    // In place: S[k][k] <- d_k, S[i][k] (i > k) keeps L_ik d_k.
+    bool chol_fail = false;
     for (int k = 0; k < C; ++k) {
-      if (tid == 0) {
-        T d = sm.S[tri_idx(k, k)];
-        if (!(d > T(0)) || !isfinite((double)d)) s_flag = 1;
-        else sm.S[tri_idx(k, k)] = sqrt(d);
+      const T d = sm.S[tri_idx(k, k)];
+      if (!(d > T(0)) || !isfinite((double)d)) {
+        chol_fail = true;  // every thread reads the same pivot: uniform exit
+        break;
       }
-      __syncthreads();
-      if (s_flag) break;
-      const T dkk = sm.S[tri_idx(k, k)];
-      const T idkk = T(1) / dkk;
-      for (int i = k + 1 + tid; i < C; i += blockDim.x) sm.S[tri_idx(i, k)] *= idkk;
-      __syncthreads();
+      const T inv = T(1) / d;
       for (int i = k + 1 + wid; i < C; i += kWarps) {
-        const T lik = sm.S[tri_idx(i, k)];
+        const T lik = sm.S[tri_idx(i, k)] * inv;
         T* row = sm.S + tri_idx(i, 0);
         for (int j = k + 1 + lane; j <= i; j += 32) row[j] -= lik * sm.S[tri_idx(j, k)];
       }
       __syncthreads();
     }
-    const bool chol_fail = s_flag != 0 || (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull));
-    __syncthreads();
-    if (tid == 0) s_flag = 0;
+    if (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull)) chol_fail = true;
+    PROF_MARK(PH_CHOL)
 
     if (!chol_fail) {
-      // forward / back substitution in warp 0
+      // forward (unit L), diagonal, back substitution in warp 0
       if (wid == 0) {
         for (int k = 0; k < C; ++k) {
-          T yk = sm.rhs[k] / sm.S[tri_idx(k, k)];
+          const T wk = sm.rhs[k] / sm.S[tri_idx(k, k)];
           __syncwarp();
-          if (lane == 0) sm.rhs[k] = yk;
-          for (int i = k + 1 + lane; i < C; i += 32) sm.rhs[i] -= sm.S[tri_idx(i, k)] * yk;
+          for (int i = k + 1 + lane; i < C; i += 32) sm.rhs[i] -= sm.S[tri_idx(i, k)] * wk;
           __syncwarp();
         }
         for (int k = C - 1; k >= 0; --k) {
-          T xk = sm.rhs[k] / sm.S[tri_idx(k, k)];
+          const T xk = sm.rhs[k] / sm.S[tri_idx(k, k)];
           __syncwarp();
           if (lane == 0) sm.rhs[k] = xk;
           const T* row = sm.S + tri_idx(k, 0);
@@ -578,13 +679,14 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
           for (int k = ptr[p]; k < ptr[p + 1]; ++k) {
             const int s = sm.slot[obs_cam(obs, k)];
             if (s < 0) continue;
-            const T* Y = Ybuf + (size_t)k * kYStride;
+            T y[18];
+            load18(Ybuf + (size_t)k * kYStride, y);
 #pragma unroll
             for (int r = 0; r < 6; ++r) {
-              const T d = T(sm.dc[6 * s + r]);
-              u0 += Y[r * 3 + 0] * d;
-              u1 += Y[r * 3 + 1] * d;
-              u2 += Y[r * 3 + 2] * d;
+              const T dd = T(sm.dc[6 * s + r]);
+              u0 += y[r * 3 + 0] * dd;
+              u1 += y[r * 3 + 1] * dd;
+              u2 += y[r * 3 + 2] * dd;
             }
           }
           const T L00 = pw[0], L10 = pw[1], L11 = pw[2], L20 = pw[3], L21 = pw[4], L22 = pw[5];
@@ -598,6 +700,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       }
       __syncthreads();
     }
+    PROF_MARK(PH_SOLVE)
 
     // ---------- K5 trials, accept / reject, lambda (miniba.py:244-293) ----------
     if (tid == 0) lambdas[it] = lam;
@@ -631,6 +734,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
         }
       }
     }
+    PROF_MARK(PH_TRIAL)
     if (tid == 0) evals[it] = (uint8_t)tries;
     bool stop = false;
     if (took >= 0) {
@@ -666,6 +770,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     if (tid == 0) costs[it + 1] = cost;
     ++it;
     __syncthreads();
+    PROF_MARK(PH_COMMIT)
     if (stop) break;
   }
 
@@ -681,6 +786,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     O.final_stats[4 * b + 2] = se2;
     O.final_stats[4 * b + 3] = (double)K;
   }
+  PROF_FLUSH
   __syncthreads();
 }
 
@@ -705,14 +811,14 @@ static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutput
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = smem_bytes<T>(d->max_cams);
-  if (smem > 200 * 1024) return MBA_ERR_TOO_LARGE;
+  if (smem > 200 * 1024 || d->max_cams > 255) return MBA_ERR_TOO_LARGE;
   cudaFuncSetAttribute(solve_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<T>, kThreads, smem);
   if (per_sm < 1) return MBA_ERR_TOO_LARGE;
   int grid = n_sm * per_sm;
   if (grid > d->n_problems) grid = d->n_problems;
-  const size_t slot = ws_slot_bytes<T>(d->max_obs, d->max_points);
+  const size_t slot = ws_slot_bytes<T>(d->max_obs, d->max_points, d->max_pairs);
   if (ws_bytes < 256 + slot * (size_t)grid) return MBA_ERR_INVALID;
   SolveParams P;
   P.d = *d;
@@ -733,13 +839,19 @@ extern "C" {
 
 int32_t mba_abi_version(void) { return MBA_ABI_VERSION; }
 
+#ifdef MBA_PHASE_PROF
+int32_t mba_debug_set_phase_buffer(unsigned long long* dev_buf) {
+  return cudaMemcpyToSymbol(mba::g_prof, &dev_buf, sizeof(dev_buf)) == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
+}
+#endif
+
 size_t mba_workspace_bytes(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
   int dev = 0, n_sm = 0;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n_sm = 148;
   const bool f64 = cfg->precision == MBA_LIN_F64;
-  const size_t slot = f64 ? mba::ws_slot_bytes<double>(d->max_obs, d->max_points)
-                          : mba::ws_slot_bytes<float>(d->max_obs, d->max_points);
+  const size_t slot = f64 ? mba::ws_slot_bytes<double>(d->max_obs, d->max_points, d->max_pairs)
+                          : mba::ws_slot_bytes<float>(d->max_obs, d->max_points, d->max_pairs);
   size_t grid = (size_t)n_sm * 8;  // upper bound on resident CTAs
   if (grid > (size_t)d->n_problems) grid = d->n_problems;
   return 256 + slot * grid;
@@ -750,7 +862,8 @@ int32_t mba_solve(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutput
   if (!d || !cfg || !o || d->n_problems < 0 || cfg->max_iters < 0) return MBA_ERR_INVALID;
   if (d->n_problems == 0) return MBA_OK;
   if (d->max_cams < 1 || d->max_obs < 1) return MBA_ERR_EMPTY;
-  if (d->max_obs > 0x7fffffff || d->max_points > 0x7ffffffe) return MBA_ERR_TOO_LARGE;
+  if (d->max_obs > 0x7fffffff || d->max_points > 0x7ffffffe || d->max_pairs > 0x7fffffff)
+    return MBA_ERR_TOO_LARGE;
   cudaStream_t st = (cudaStream_t)stream;
   if (cfg->precision == MBA_LIN_F64) return mba::launch<double>(d, cfg, o, ws, ws_bytes, st);
   return mba::launch<float>(d, cfg, o, ws, ws_bytes, st);

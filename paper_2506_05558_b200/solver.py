@@ -34,6 +34,7 @@ class HostBatch:
     t: np.ndarray
     focal: np.ndarray
     points: np.ndarray
+    max_pairs: int = 0
 
     @property
     def n_problems(self):
@@ -50,6 +51,16 @@ class HostBatch:
     @property
     def max_points(self):
         return int(np.max(np.diff(self.pt_off))) if self.n_problems else 0
+
+
+def _max_pairs(obs_off, pt_off, pt):
+    """max over problems of sum_p m_p (m_p + 1) / 2 (co-observation pairs)."""
+    n_obs = np.diff(obs_off)
+    gpt = np.repeat(pt_off[:-1], n_obs) + pt
+    m = np.bincount(gpt, minlength=int(pt_off[-1])).astype(np.int64)
+    per_pt = m * (m + 1) // 2
+    prob = np.repeat(np.arange(len(n_obs)), np.diff(pt_off))
+    return int(np.bincount(prob, weights=per_pt, minlength=len(n_obs)).max()) if len(n_obs) else 0
 
 
 def _records(uv, cam, pt):
@@ -99,11 +110,14 @@ def pack_problems(problems) -> HostBatch:
         fl.append((1 if of else 0) | (2 if op else 0))
     off = lambda v: np.concatenate([[0], np.cumsum(v)]).astype(np.int64)
     lo = np.concatenate(los)
-    return HostBatch(cam_off=off(n_c), pt_off=off(n_p), obs_off=off(n_o), obs=np.concatenate(recs),
+    obs = np.concatenate(recs)
+    pt_off, obs_off = off(n_p), off(n_o)
+    return HostBatch(cam_off=off(n_c), pt_off=pt_off, obs_off=obs_off, obs=obs,
                      obs_lo=lo if np.any(lo) else None, fixed=np.concatenate(fixed),
                      cx=np.array(cx), cy=np.array(cy), flags=np.array(fl, dtype=np.uint8),
                      R=np.concatenate(Rs), t=np.concatenate(ts), focal=np.array(foc),
-                     points=np.concatenate(pts))
+                     points=np.concatenate(pts),
+                     max_pairs=_max_pairs(obs_off, pt_off, obs.view(np.int32)[:, 3]))
 
 
 def pack_synth(b) -> HostBatch:
@@ -113,7 +127,8 @@ def pack_synth(b) -> HostBatch:
                     dtype=np.uint8)
     return HostBatch(cam_off=b.cam_off, pt_off=b.pt_off, obs_off=b.obs_off, obs=rec,
                      obs_lo=lo if np.any(lo) else None, fixed=b.fixed.astype(np.uint8), cx=b.cx,
-                     cy=b.cy, flags=flags, R=b.R, t=b.t, focal=b.focal, points=b.points)
+                     cy=b.cy, flags=flags, R=b.R, t=b.t, focal=b.focal, points=b.points,
+                     max_pairs=_max_pairs(b.obs_off, b.pt_off, b.pt))
 
 
 @dataclass
@@ -122,6 +137,7 @@ class DeviceBatch:
     max_cams: int
     max_obs: int
     max_points: int
+    max_pairs: int
     cam_off: object
     pt_off: object
     obs_off: object
@@ -168,7 +184,7 @@ def to_device(hb: HostBatch, device=None, pinned=None) -> DeviceBatch:
         d[k] = a.to(dev, non_blocking=True)
         nbytes += a.numel() * a.element_size()
     return DeviceBatch(n_problems=hb.n_problems, max_cams=hb.max_cams, max_obs=hb.max_obs,
-                       max_points=hb.max_points, h2d_bytes=nbytes, **d)
+                       max_points=hb.max_points, max_pairs=hb.max_pairs, h2d_bytes=nbytes, **d)
 
 
 @dataclass
@@ -178,14 +194,14 @@ class LmParams:
     delta: float = 2.0
     max_iters: int = 200
     loss: str = "huber"
-    precision: str = "mixed"
+    precision: str = "f64"
     fail_at: tuple = ()
 
     @staticmethod
     def from_cfg(cfg, **over):
         p = LmParams(lambda_init=cfg.lambda_init, nu=cfg.nu, delta=cfg.huber_delta,
                      max_iters=cfg.max_iters, loss=getattr(cfg, "loss", "huber"),
-                     precision=getattr(cfg, "precision", "mixed"))
+                     precision=getattr(cfg, "precision", "f64"))
         for k, v in over.items():
             setattr(p, k, v)
         return p
@@ -231,7 +247,7 @@ def _workspace(nbytes, device):
 
 def descriptors(db: DeviceBatch, prm: LmParams, sol: Solution):
     d = MbaBatchDesc(n_problems=db.n_problems, max_cams=db.max_cams, max_obs=db.max_obs,
-                     max_points=db.max_points, cam_off=ptr(db.cam_off), pt_off=ptr(db.pt_off),
+                     max_points=db.max_points, max_pairs=db.max_pairs, cam_off=ptr(db.cam_off), pt_off=ptr(db.pt_off),
                      obs_off=ptr(db.obs_off), obs=ptr(db.obs), obs_lo=ptr(db.obs_lo),
                      fixed=ptr(db.fixed), cx=ptr(db.cx), cy=ptr(db.cy), flags=ptr(db.flags))
     c = MbaLmConfig(lambda_init=prm.lambda_init, nu=prm.nu, delta=prm.delta,

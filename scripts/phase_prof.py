@@ -1,0 +1,55 @@
+"""Per-phase cycle breakdown of mba::solve_kernel (profiling build).
+
+    python paper_2506_05558_b200/build.py --prof
+    python scripts/phase_prof.py --config 4 --problems 8192 [--precision mixed]
+"""
+import argparse
+import ctypes as ct
+import json
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [REPO, os.path.join(REPO, "src")]
+os.environ["MBA_LIB"] = os.path.join(REPO, "paper_2506_05558_b200", "libminiba_prof.so")
+
+PHASES = ["setup", "cost0", "point", "jobs", "assemble", "cholesky", "solve+backsub", "trials", "commit"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--problems", type=int, default=8192)
+    ap.add_argument("--precision", default="mixed")
+    a = ap.parse_args()
+    import torch
+    from paper_2506_05558_b200 import _lib, solver
+    from paper_2506_05558_b200.synth import CONFIGS, make_batch
+    c = CONFIGS[a.config]
+    n = min(a.problems, c["n_problems"])
+    b = make_batch(n, n_cams=c["n_cams"], K=c["K"], outlier_frac=c.get("outlier_frac", 0.0),
+                   workers=os.cpu_count())
+    db = solver.to_device(solver.pack_synth(b))
+    prm = solver.LmParams(max_iters=c["max_iters"], loss=c["loss"], precision=a.precision)
+    L = _lib.lib()
+    buf = torch.zeros(16, dtype=torch.int64, device="cuda")
+    L.mba_debug_set_phase_buffer.argtypes = [ct.c_void_p]
+    sol = solver.solve(db, prm)
+    torch.cuda.synchronize()
+    L.mba_debug_set_phase_buffer(ct.c_void_p(buf.data_ptr()))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    solver.solve(db, prm, sol)
+    ev[1].record()
+    torch.cuda.synchronize()
+    cyc = buf.cpu().numpy()[:len(PHASES)].astype(float)
+    tot = cyc.sum()
+    iters = float(sol.n_iters.sum().item())
+    out = {"config": a.config, "problems": n, "precision": a.precision, "ms": ev[0].elapsed_time(ev[1]),
+           "lm_iters": iters,
+           "phases": {p: {"frac": c_ / tot, "cycles_per_problem_iter": c_ / iters} for p, c_ in zip(PHASES, cyc)}}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
