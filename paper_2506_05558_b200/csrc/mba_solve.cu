@@ -74,81 +74,55 @@ struct SolveParams {
   int max_cams;
 };
 
-template <typename T>
-struct Smem {
-  double* Rc;   // [n][9] current rotations
-  double* tc;   // [n][3]
-  double* Rt;   // [n][9] trial
-  double* tt;   // [n][3]
-  double* dc;   // [Cmax] step (double copy)
-  double* red;  // [kWarps * 4]
-  T* S;         // packed lower [Cmax(Cmax+1)/2]
-  T* rhs;       // [Cmax]
-  T* ucam;      // [nfmax * kUcamStride]
-  int* cam_ptr; // [n+1]
-  int* slot;    // [n]
-  int* cam_of_slot;  // [n]
-  int* blk_off;      // [nbmax+1] pair-list offsets per camera block
-  unsigned char* blk_a;  // [nbmax] block -> (slot a, slot b)
-  unsigned char* blk_b;
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Compile-time shared-memory layout for problems of up to MAXC cameras.
+// The fixed part holds the camera state, the packed reduced camera system and
+// the small index tables; in resident mode the per-problem scratch (camera
+// permutation, point CSR, pair list, Y blocks, point factors) follows it, so
+// the whole LM iteration runs out of shared memory.
+template <typename T, int MAXC>
+struct Layout {
+  static constexpr int N = MAXC, C = 6 * MAXC + 1, NB = MAXC * (MAXC + 1) / 2;
+  static constexpr size_t oRc = 0;                                  // double[N][9]
+  static constexpr size_t oTc = oRc + 8 * 9 * N;                    // double[N][3]
+  static constexpr size_t oRt = oTc + 8 * 3 * N;                    // trial
+  static constexpr size_t oTt = oRt + 8 * 9 * N;
+  static constexpr size_t oDc = oTt + 8 * 3 * N;                    // double[C]
+  static constexpr size_t oRed = align16(oDc + 8 * C);              // double[kWarps*4]
+  static constexpr size_t oS = oRed + 8 * kWarps * 4;               // T[C(C+1)/2]
+  static constexpr size_t oRhs = align16(oS + sizeof(T) * C * (C + 1) / 2);
+  static constexpr size_t oUcam = align16(oRhs + sizeof(T) * C);    // T[N][kUcamStride]
+  static constexpr size_t oCamPtr = align16(oUcam + sizeof(T) * N * kUcamStride);
+  static constexpr size_t oSlot = oCamPtr + 4 * (N + 1);
+  static constexpr size_t oCos = oSlot + 4 * N;
+  static constexpr size_t oBlkOff = oCos + 4 * N;                   // int[NB+1]
+  static constexpr size_t oBlkA = oBlkOff + 4 * (NB + 1);           // uchar[NB]
+  static constexpr size_t oBlkB = oBlkA + NB;
+  static constexpr size_t kFixed = align16(oBlkB + NB);
 };
 
-__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-
-template <typename T>
-__host__ __device__ inline size_t smem_bytes(int max_cams) {
-  size_t n = max_cams, C = 6 * n + 1, nb = n * (n + 1) / 2;
-  size_t b = 0;
-  b += align16(sizeof(double) * n * 24);
-  b += align16(sizeof(double) * C);
-  b += align16(sizeof(double) * kWarps * 4);
-  b += align16(sizeof(T) * C * (C + 1) / 2);
-  b += align16(sizeof(T) * C);
-  b += align16(sizeof(T) * n * kUcamStride);
-  b += align16(sizeof(int) * (n + 1));
-  b += align16(sizeof(int) * n * 2);
-  b += align16(sizeof(int) * (nb + 1));
-  b += align16(2 * nb);
-  return b;
-}
-
-template <typename T>
-__device__ inline Smem<T> carve(unsigned char* base, int max_cams) {
-  Smem<T> s;
-  size_t n = max_cams, C = 6 * n + 1, nb = n * (n + 1) / 2, off = 0;
-  auto take = [&](size_t bytes) { unsigned char* p = base + off; off += align16(bytes); return p; };
-  double* cams = (double*)take(sizeof(double) * n * 24);
-  s.Rc = cams;
-  s.tc = cams + 9 * n;
-  s.Rt = cams + 12 * n;
-  s.tt = cams + 21 * n;
-  s.dc = (double*)take(sizeof(double) * C);
-  s.red = (double*)take(sizeof(double) * kWarps * 4);
-  s.S = (T*)take(sizeof(T) * C * (C + 1) / 2);
-  s.rhs = (T*)take(sizeof(T) * C);
-  s.ucam = (T*)take(sizeof(T) * n * kUcamStride);
-  s.cam_ptr = (int*)take(sizeof(int) * (n + 1));
-  int* sl = (int*)take(sizeof(int) * n * 2);
-  s.slot = sl;
-  s.cam_of_slot = sl + n;
-  s.blk_off = (int*)take(sizeof(int) * (nb + 1));
-  s.blk_a = (unsigned char*)take(2 * nb);
-  s.blk_b = s.blk_a + nb;
-  return s;
-}
-
-template <typename T>
-__host__ __device__ inline size_t ws_slot_bytes(int64_t max_obs, int64_t max_points, int64_t max_pairs) {
-  size_t b = 0;
-  b += align16(sizeof(int) * max_obs);              // camera-major permutation
-  b += align16(sizeof(int) * (max_points + 1));     // point CSR
-  b += align16(sizeof(int2) * max_pairs);           // pair lists
-  b += align16(sizeof(T) * kYStride * max_obs);     // W_i / Y_i
-  b += align16(sizeof(T) * kPtStride * max_points); // per-point factors
-  return b;
-}
-
 // ---- vector helpers for the 18-value Y blocks ------------------------------
+// Y rows are stored with stride kYStride (20, 16-byte vectors) in global
+// scratch and kYStrideRes (18, 8-byte vectors) in shared-memory scratch.
+constexpr int kYStrideRes = 18;
+
+template <bool RES> struct YS { static constexpr int v = RES ? kYStrideRes : kYStride; };
+
+__device__ __forceinline__ void load18v2(const float* p, float y[18]) {
+  const float2* q = reinterpret_cast<const float2*>(p);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    float2 v = q[i];
+    y[2 * i] = v.x;
+    y[2 * i + 1] = v.y;
+  }
+}
+__device__ __forceinline__ void store18v2(float* p, const float y[18]) {
+  float2* q = reinterpret_cast<float2*>(p);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) q[i] = make_float2(y[2 * i], y[2 * i + 1]);
+}
 
 __device__ __forceinline__ void load18(const float* p, float y[18]) {
   const float4* q = reinterpret_cast<const float4*>(p);
@@ -267,16 +241,78 @@ __device__ void cost_pass(const MbaObs* __restrict__ obs, const float* __restric
   out[2] = acc[2];
 }
 
-template <typename T>
+// Per-problem scratch: in shared memory (RES) or in this CTA's global slot.
+template <typename T, bool RES>
+struct Scratch {
+  int* perm;        // camera-major permutation of the observations
+  int* ptr;         // point CSR
+  void* pairs;      // RES: uint32 (i << 16 | j); else int2
+  T* Ybuf;          // [K][kYStride]
+  T* ptw;           // [P][kPtStride]
+  __device__ __forceinline__ int2 pair(int q) const {
+    if (RES) {
+      const unsigned v = static_cast<const unsigned*>(pairs)[q];
+      return make_int2((int)(v >> 16), (int)(v & 0xffffu));
+    }
+    return static_cast<const int2*>(pairs)[q];
+  }
+  __device__ __forceinline__ void set_pair(int q, int i, int j) const {
+    if (RES) static_cast<unsigned*>(pairs)[q] = ((unsigned)i << 16) | (unsigned)j;
+    else static_cast<int2*>(pairs)[q] = make_int2(i, j);
+  }
+};
+
+template <typename T, bool RES>
+__host__ __device__ inline size_t scratch_bytes(int64_t max_obs, int64_t max_points, int64_t max_pairs) {
+  return align16(sizeof(int) * max_obs) + align16(sizeof(int) * (max_points + 1)) +
+         align16((RES ? 4 : 8) * max_pairs) + align16(sizeof(T) * YS<RES>::v * max_obs) +
+         align16(sizeof(T) * kPtStride * max_points);
+}
+
+template <typename T, bool RES>
+__device__ __forceinline__ Scratch<T, RES> scratch_at(unsigned char* base, const MbaBatchDesc& D) {
+  Scratch<T, RES> w;
+  w.perm = (int*)base;
+  w.ptr = (int*)(base + align16(sizeof(int) * D.max_obs));
+  unsigned char* q = (unsigned char*)w.ptr + align16(sizeof(int) * (D.max_points + 1));
+  w.pairs = q;
+  q += align16((RES ? 4 : 8) * D.max_pairs);
+  w.Ybuf = (T*)q;
+  w.ptw = (T*)(q + align16(sizeof(T) * YS<RES>::v * D.max_obs));
+  return w;
+}
+
+template <typename T, int MAXC, bool RES>
 __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) {
+  using L = Layout<T, MAXC>;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const MbaBatchDesc& D = P.d;
   const MbaLmConfig& cfg = P.cfg;
   const MbaOutputs& O = P.o;
-  Smem<T> sm = carve<T>(smem_raw, P.max_cams);
+  struct {
+    double *Rc, *tc, *Rt, *tt, *dc, *red;
+    T *S, *rhs, *ucam;
+    int *cam_ptr, *slot, *cam_of_slot, *blk_off;
+    unsigned char *blk_a, *blk_b;
+  } sm;
+  sm.Rc = (double*)(smem_raw + L::oRc);
+  sm.tc = (double*)(smem_raw + L::oTc);
+  sm.Rt = (double*)(smem_raw + L::oRt);
+  sm.tt = (double*)(smem_raw + L::oTt);
+  sm.dc = (double*)(smem_raw + L::oDc);
+  sm.red = (double*)(smem_raw + L::oRed);
+  sm.S = (T*)(smem_raw + L::oS);
+  sm.rhs = (T*)(smem_raw + L::oRhs);
+  sm.ucam = (T*)(smem_raw + L::oUcam);
+  sm.cam_ptr = (int*)(smem_raw + L::oCamPtr);
+  sm.slot = (int*)(smem_raw + L::oSlot);
+  sm.cam_of_slot = (int*)(smem_raw + L::oCos);
+  sm.blk_off = (int*)(smem_raw + L::oBlkOff);
+  sm.blk_a = smem_raw + L::oBlkA;
+  sm.blk_b = smem_raw + L::oBlkB;
   __shared__ int s_flag;        // setup error
   __shared__ int s_C, s_nf;
-  __shared__ double s_red4[kWarps * 4];
+  double* s_red4 = sm.red;
 
   const int64_t cb = D.cam_off[b], pb = D.pt_off[b], ob = D.obs_off[b];
   const int n = (int)(D.cam_off[b + 1] - cb);
@@ -291,12 +327,19 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   const float* __restrict__ lo = D.obs_lo ? D.obs_lo + 2 * ob : nullptr;
   double* __restrict__ X = O.points_out + 3 * pb;
 
-  unsigned char* ws = P.ws + (size_t)blockIdx.x * P.ws_slot_bytes;
-  int* perm = (int*)ws;
-  int* ptr = (int*)(ws + align16(sizeof(int) * D.max_obs));
-  int2* pairs = (int2*)((unsigned char*)ptr + align16(sizeof(int) * (D.max_points + 1)));
-  T* Ybuf = (T*)((unsigned char*)pairs + align16(sizeof(int2) * D.max_pairs));
-  T* ptw = (T*)((unsigned char*)Ybuf + align16(sizeof(T) * kYStride * D.max_obs));
+  const Scratch<T, RES> W = scratch_at<T, RES>(
+      RES ? smem_raw + L::kFixed : P.ws + (size_t)blockIdx.x * P.ws_slot_bytes, D);
+  constexpr int YSTR = YS<RES>::v;
+  auto ld18 = [](const T* p, T y[18]) {
+    if constexpr (RES && sizeof(T) == 4) load18v2((const float*)p, (float*)y); else load18(p, y);
+  };
+  auto st18 = [](T* p, const T y[18]) {
+    if constexpr (RES && sizeof(T) == 4) store18v2((float*)p, (const float*)y); else store18(p, y);
+  };
+  int* __restrict__ perm = W.perm;
+  int* __restrict__ ptr = W.ptr;
+  T* __restrict__ Ybuf = W.Ybuf;
+  T* __restrict__ ptw = W.ptw;
 
   double* costs = O.costs + (size_t)b * (max_it + 1);
   double* lambdas = O.lambdas + (size_t)b * max_it;
@@ -393,7 +436,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
         if (pass) {
           int pos = base + warp_excl_scan(m, lane);
           for (int j = j0; j < j1 && m; ++j)
-            if (obs_cam(obs, j) == cbb) pairs[pos++] = make_int2(i, j);
+            if (obs_cam(obs, j) == cbb) W.set_pair(pos++, i, j);
         }
         base += warp_sum(m);
       }
@@ -474,7 +517,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
             for (int r = 0; r < 6; ++r)
 #pragma unroll
               for (int a = 0; a < 3; ++a) W[r * 3 + a] = A[r] * wB[a] + A[6 + r] * wB[3 + a];
-            store18(Ybuf + (size_t)k * kYStride, W);
+            st18(Ybuf + (size_t)k * YSTR, W);
           }
         }
       }
@@ -493,9 +536,9 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       T i22 = T(1) / L22;
       for (int k = k0; k < k1; ++k) {
         if (sm.slot[obs_cam(obs, k)] < 0) continue;
-        T* Wk = Ybuf + (size_t)k * kYStride;
+        T* Wk = Ybuf + (size_t)k * YSTR;
         T y[18];
-        load18(Wk, y);
+        ld18(Wk, y);
 #pragma unroll
         for (int r = 0; r < 6; ++r) {
           T y0 = y[r * 3 + 0] * i00;
@@ -505,7 +548,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
           y[r * 3 + 1] = y1;
           y[r * 3 + 2] = y2;
         }
-        store18(Wk, y);
+        st18(Wk, y);
       }
       T z0 = g[0] * i00, z1 = (g[1] - L10 * z0) * i11, z2 = (g[2] - L20 * z0 - L21 * z1) * i22;
       T f0 = wf[0] * i00, f1 = (wf[1] - L10 * f0) * i11, f2 = (wf[2] - L20 * f0 - L21 * f1) * i22;
@@ -553,7 +596,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
           }
           if (opt_pts) {
             T y[18];
-            load18(Ybuf + (size_t)k * kYStride, y);
+            ld18(Ybuf + (size_t)k * YSTR, y);
             const T* pw = ptw + (size_t)o.pt * kPtStride;
             const T z0 = pw[6], z1 = pw[7], z2 = pw[8], f0 = pw[9], f1 = pw[10], f2 = pw[11];
 #pragma unroll
@@ -575,10 +618,10 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
         for (int i = 0; i < 36; ++i) acc[i] = T(0);
         const int q1 = sm.blk_off[blk + 1];
         for (int q = sm.blk_off[blk] + lane; q < q1; q += 32) {
-          const int2 pr = pairs[q];
+          const int2 pr = W.pair(q);
           T yi[18], yj[18];
-          load18(Ybuf + (size_t)pr.x * kYStride, yi);
-          load18(Ybuf + (size_t)pr.y * kYStride, yj);
+          ld18(Ybuf + (size_t)pr.x * YSTR, yi);
+          ld18(Ybuf + (size_t)pr.y * YSTR, yj);
 #pragma unroll
           for (int r = 0; r < 6; ++r)
 #pragma unroll
@@ -680,7 +723,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
             const int s = sm.slot[obs_cam(obs, k)];
             if (s < 0) continue;
             T y[18];
-            load18(Ybuf + (size_t)k * kYStride, y);
+            ld18(Ybuf + (size_t)k * YSTR, y);
 #pragma unroll
             for (int r = 0; r < 6; ++r) {
               const T dd = T(sm.dc[6 * s + r]);
@@ -790,8 +833,8 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   __syncthreads();
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) solve_kernel(SolveParams P) {
+template <typename T, int MAXC, bool RES>
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && !RES) ? 2 : 1) solve_kernel(SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_prob;
   for (;;) {
@@ -800,37 +843,62 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) solve_kernel
     const int b = s_prob;
     __syncthreads();
     if (b >= P.d.n_problems) return;
-    solve_one<T>(P, b, smem_raw);
+    solve_one<T, MAXC, RES>(P, b, smem_raw);
   }
 }
 
-template <typename T>
-static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
-                  size_t ws_bytes, cudaStream_t st) {
+constexpr size_t kSmemLimit = 227 * 1024;
+
+template <typename T, int MAXC, bool RES>
+static int launch_cfg(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
+                      size_t ws_bytes, cudaStream_t st) {
   int dev = 0, n_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = smem_bytes<T>(d->max_cams);
-  if (smem > 200 * 1024 || d->max_cams > 255) return MBA_ERR_TOO_LARGE;
-  cudaFuncSetAttribute(solve_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t scratch = scratch_bytes<T, RES>(d->max_obs, d->max_points, d->max_pairs);
+  const size_t smem = Layout<T, MAXC>::kFixed + (RES ? scratch : 0);
+  if (smem > kSmemLimit) return MBA_ERR_TOO_LARGE;
+  cudaFuncSetAttribute(solve_kernel<T, MAXC, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<T>, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<T, MAXC, RES>, kThreads, smem);
   if (per_sm < 1) return MBA_ERR_TOO_LARGE;
   int grid = n_sm * per_sm;
   if (grid > d->n_problems) grid = d->n_problems;
-  const size_t slot = ws_slot_bytes<T>(d->max_obs, d->max_points, d->max_pairs);
-  if (ws_bytes < 256 + slot * (size_t)grid) return MBA_ERR_INVALID;
+  if (!RES && ws_bytes < 256 + scratch * (size_t)grid) return MBA_ERR_INVALID;
   SolveParams P;
   P.d = *d;
   P.cfg = *cfg;
   P.o = *o;
   P.counter = (int*)ws;
   P.ws = (unsigned char*)ws + 256;
-  P.ws_slot_bytes = slot;
+  P.ws_slot_bytes = scratch;
   P.max_cams = d->max_cams;
   cudaMemsetAsync(ws, 0, sizeof(int), st);
-  solve_kernel<T><<<grid, kThreads, smem, st>>>(P);
+  solve_kernel<T, MAXC, RES><<<grid, kThreads, smem, st>>>(P);
   return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
+}
+
+// Shared-memory-resident scratch when the largest problem of the batch fits,
+// else scratch in a per-CTA global slot (L2-resident for moderate sizes).
+template <typename T, int MAXC>
+static bool resident_fits(const MbaBatchDesc* d) {
+  return d->max_obs < 65536 &&
+         Layout<T, MAXC>::kFixed + scratch_bytes<T, true>(d->max_obs, d->max_points, d->max_pairs) <= kSmemLimit;
+}
+
+template <typename T>
+static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
+                  size_t ws_bytes, cudaStream_t st) {
+  if (d->max_cams <= 8) {
+    if (resident_fits<T, 8>(d)) return launch_cfg<T, 8, true>(d, cfg, o, ws, ws_bytes, st);
+    return launch_cfg<T, 8, false>(d, cfg, o, ws, ws_bytes, st);
+  }
+  if (d->max_cams <= 16) {
+    if (resident_fits<T, 16>(d)) return launch_cfg<T, 16, true>(d, cfg, o, ws, ws_bytes, st);
+    return launch_cfg<T, 16, false>(d, cfg, o, ws, ws_bytes, st);
+  }
+  if (d->max_cams <= 32) return launch_cfg<T, 32, false>(d, cfg, o, ws, ws_bytes, st);
+  return MBA_ERR_TOO_LARGE;
 }
 
 }  // namespace mba
@@ -850,8 +918,8 @@ size_t mba_workspace_bytes(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n_sm = 148;
   const bool f64 = cfg->precision == MBA_LIN_F64;
-  const size_t slot = f64 ? mba::ws_slot_bytes<double>(d->max_obs, d->max_points, d->max_pairs)
-                          : mba::ws_slot_bytes<float>(d->max_obs, d->max_points, d->max_pairs);
+  const size_t slot = f64 ? mba::scratch_bytes<double, false>(d->max_obs, d->max_points, d->max_pairs)
+                          : mba::scratch_bytes<float, false>(d->max_obs, d->max_points, d->max_pairs);
   size_t grid = (size_t)n_sm * 8;  // upper bound on resident CTAs
   if (grid > (size_t)d->n_problems) grid = d->n_problems;
   return 256 + slot * grid;
