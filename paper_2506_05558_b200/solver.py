@@ -196,6 +196,7 @@ class LmParams:
     loss: str = "huber"
     precision: str = "f64"
     fail_at: tuple = ()
+    kernel: str = "auto"      # "auto" | "warp" (one warp per problem) | "cta" (one CTA per problem)
 
     @staticmethod
     def from_cfg(cfg, **over):
@@ -252,7 +253,8 @@ def descriptors(db: DeviceBatch, prm: LmParams, sol: Solution):
                      fixed=ptr(db.fixed), cx=ptr(db.cx), cy=ptr(db.cy), flags=ptr(db.flags))
     c = MbaLmConfig(lambda_init=prm.lambda_init, nu=prm.nu, delta=prm.delta,
                     max_iters=prm.max_iters, loss=_lib.LOSS[prm.loss],
-                    precision=_lib.PRECISION[prm.precision], ctas_per_problem=0,
+                    precision=_lib.PRECISION[prm.precision],
+                    ctas_per_problem={"auto": 0, "warp": -1, "cta": -2}[prm.kernel],
                     fail_iters_mask=sum(1 << int(i) for i in prm.fail_at if 0 <= int(i) < 64))
     o = MbaOutputs(R_in=ptr(db.R), t_in=ptr(db.t), focal_in=ptr(db.focal), points_in=ptr(db.points),
                    R_out=ptr(sol.R), t_out=ptr(sol.t), focal_out=ptr(sol.focal),

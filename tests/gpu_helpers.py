@@ -11,14 +11,14 @@ ROT_TOL = 1e-4
 TRANS_RTOL = 1e-4
 
 
-def run_device(problems, lm_cfg, precision="mixed"):
+def run_device(problems, lm_cfg, precision="mixed", kernel="auto"):
     from paper_2506_05558_b200 import solver
     hb = solver.pack_problems(problems)
     db = solver.to_device(hb)
     prm = solver.LmParams(lambda_init=lm_cfg.get("lambda_init", 1e-5), nu=lm_cfg.get("nu", 2.0),
                           delta=lm_cfg.get("delta", 2.0), max_iters=lm_cfg.get("max_iters", 200),
                           loss=lm_cfg.get("loss", "huber"), precision=precision,
-                          fail_at=tuple(lm_cfg.get("fail_at", ())))
+                          fail_at=tuple(lm_cfg.get("fail_at", ())), kernel=kernel)
     sol = solver.solve(db, prm)
     R, t, f, X = (sol.R.cpu().numpy(), sol.t.cpu().numpy(), sol.focal.cpu().numpy(),
                   sol.points.cpu().numpy())
