@@ -68,6 +68,8 @@ typedef struct {
   int64_t max_points;        /* max points in any problem             */
   int64_t max_pairs;         /* max over problems of sum_p m_p (m_p + 1) / 2, m_p =
                                 observations of point p (co-observation pairs)  */
+  int32_t max_track;         /* max observations of any single point           */
+  int32_t reserved;
   const int64_t* cam_off;    /* camera rows of problem b: [cam_off[b], cam_off[b+1]) */
   const int64_t* pt_off;
   const int64_t* obs_off;

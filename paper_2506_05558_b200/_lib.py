@@ -23,7 +23,8 @@ _vp = ct.c_void_p
 
 class MbaBatchDesc(ct.Structure):
     _fields_ = [("n_problems", ct.c_int32), ("max_cams", ct.c_int32), ("max_obs", ct.c_int64),
-                ("max_points", ct.c_int64), ("max_pairs", ct.c_int64), ("cam_off", _vp), ("pt_off", _vp), ("obs_off", _vp),
+                ("max_points", ct.c_int64), ("max_pairs", ct.c_int64),
+                ("max_track", ct.c_int32), ("reserved", ct.c_int32), ("cam_off", _vp), ("pt_off", _vp), ("obs_off", _vp),
                 ("obs", _vp), ("obs_lo", _vp), ("fixed", _vp), ("cx", _vp), ("cy", _vp),
                 ("flags", _vp)]
 

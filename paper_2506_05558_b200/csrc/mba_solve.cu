@@ -1470,6 +1470,682 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, sizeof(T) == 4 ? 4 : 2) sol
   }
 }
 
+// ===========================================================================
+// Point-wise solver (the default for problems with <= 8 cameras).
+//
+// Per point p the Schur-reduced, augmented camera system receives
+//     S_aug  +=  sum_{i in p} J_i^T w_i J_i   -   Yhat_p Yhat_p^T
+// where J_i = [A_i | F_i | -r_i] (camera columns, focal column, rhs "row" C)
+// and Yhat_p stacks the rows Y_i = W_i L_p^-T of the point's free-camera
+// observations, y_f = L_p^-1 Wf_p and -z_p = -L_p^-1 g_p (miniba.py:135-177,
+// 207-213). Every warp owns a contiguous range of points and a private copy of
+// S_aug in shared memory; it walks its range in chunks of <= 32 observations:
+//   (a) lane per observation: fp64 projection, Jacobians, per-observation V/g
+//       contributions and W_i, staged in shared memory;
+//   (b) lane per point: damped 3x3 Cholesky of V_p, z_p, y_f;
+//   (c) lane per observation: Y_i = W_i L_p^-T;
+//   (d) point by point, lanes over (observation pair, row) and (observation,
+//       row) tasks: 6x6 Schur blocks and the J^T w J rows, read-modify-write into
+//       the warp's private S_aug -- no atomics, fixed order.
+// The private copies are summed in warp order, damped, factorised (LDL^T with
+// the forward substitution fused) and back-substituted by the whole CTA; the
+// point back-substitution recomputes W_i^T dc = w B_i^T (A_i dc) instead of
+// storing Y. No per-observation scratch exists: per-CTA global scratch is
+// only the point CSR and the per-point factors.
+// ===========================================================================
+
+constexpr int kChunk = 32;   // observations per warp chunk
+constexpr int kSRow = 48;    // staged values per observation (A12 F2 r2 w1 | W/Y 18 | Vc6 gc3 wfc3)
+
+template <typename T, int MAXC, int NW>
+struct PLayout {
+  static constexpr int N = MAXC, C = 6 * MAXC + 1, CA = C * (C + 3) / 2;
+  static constexpr size_t oRc = 0;
+  static constexpr size_t oTc = oRc + 8 * 9 * N;
+  static constexpr size_t oRt = oTc + 8 * 3 * N;
+  static constexpr size_t oTt = oRt + 8 * 9 * N * kBacktrackTries;
+  static constexpr size_t oDc = oTt + 8 * 3 * N * kBacktrackTries;
+  static constexpr size_t oRed = align16(oDc + 8 * C);           // double[NW * 4]
+  static constexpr size_t oS = align16(oRed + 8 * NW * 4);        // T[CA]
+  static constexpr size_t oXs = align16(oS + sizeof(T) * CA);     // T[C]
+  static constexpr size_t oTab = align16(oXs + sizeof(T) * C);    // u16[CA]
+  static constexpr size_t oSlot = align16(oTab + 2 * CA);         // int[N]
+  static constexpr size_t oSw = align16(oSlot + 4 * N);           // T[NW][CA]
+  static constexpr size_t oUd = align16(oSw + sizeof(T) * NW * CA);   // T[NW][C]
+  static constexpr size_t oSt = align16(oUd + sizeof(T) * NW * C);    // T[NW][kChunk][kSRow]
+  static constexpr size_t oSs = align16(oSt + sizeof(T) * NW * kChunk * kSRow);  // int[NW][kChunk]
+  static constexpr size_t oPs = align16(oSs + 4 * NW * kChunk);   // T[NW][kChunk][12]
+  static constexpr size_t oPi = align16(oPs + sizeof(T) * NW * kChunk * 12);  // int[NW][kChunk][2]
+  static constexpr size_t kBytes = align16(oPi + 8 * NW * kChunk);
+};
+
+template <typename T>
+__host__ __device__ inline size_t pw_scratch_bytes(int64_t max_points) {
+  return align16(sizeof(int) * (max_points + 1)) + align16(sizeof(T) * 16 * max_points);
+}
+
+template <typename T, int MAXC, int NW>
+__device__ void pw_solve_one(const SolveParams& P, int b, unsigned char* smem_raw) {
+  using L = PLayout<T, MAXC, NW>;
+  constexpr int NT = 32 * NW;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const MbaBatchDesc& D = P.d;
+  const MbaLmConfig& cfg = P.cfg;
+  const MbaOutputs& O = P.o;
+  double* Rc = (double*)(smem_raw + L::oRc);
+  double* tc = (double*)(smem_raw + L::oTc);
+  double* Rt = (double*)(smem_raw + L::oRt);
+  double* tt = (double*)(smem_raw + L::oTt);
+  double* dcs = (double*)(smem_raw + L::oDc);
+  double* red = (double*)(smem_raw + L::oRed);
+  T* S = (T*)(smem_raw + L::oS);
+  T* xs = (T*)(smem_raw + L::oXs);
+  unsigned short* tab = (unsigned short*)(smem_raw + L::oTab);
+  int* slot = (int*)(smem_raw + L::oSlot);
+  T* Sw = (T*)(smem_raw + L::oSw) + (size_t)wid * L::CA;
+  T* Ud = (T*)(smem_raw + L::oUd) + (size_t)wid * L::C;
+  T* st = (T*)(smem_raw + L::oSt) + (size_t)wid * kChunk * kSRow;
+  int* sslot = (int*)(smem_raw + L::oSs) + wid * kChunk;
+  T* ps = (T*)(smem_raw + L::oPs) + (size_t)wid * kChunk * 12;
+  int* pi = (int*)(smem_raw + L::oPi) + wid * kChunk * 2;
+  __shared__ int s_flag;
+
+  const int64_t cb = D.cam_off[b], pb = D.pt_off[b], ob = D.obs_off[b];
+  const int n = (int)(D.cam_off[b + 1] - cb);
+  const int Pn = (int)(D.pt_off[b + 1] - pb);
+  const int K = (int)(D.obs_off[b + 1] - ob);
+  const uint8_t fl = D.flags[b];
+  const bool has_f = fl & 1, opt_pts = (fl >> 1) & 1;
+  const double cx = D.cx[b], cy = D.cy[b];
+  const double delta = cfg.delta, nu = cfg.nu;
+  const int loss = cfg.loss, max_it = cfg.max_iters;
+  const MbaObs* __restrict__ obs = D.obs + ob;
+  const float* __restrict__ lo = D.obs_lo ? D.obs_lo + 2 * ob : nullptr;
+  double* __restrict__ X = O.points_out + 3 * pb;
+  unsigned char* wsb = P.ws + (size_t)blockIdx.x * P.ws_slot_bytes;
+  int* __restrict__ ptr = (int*)wsb;
+  T* __restrict__ ptw = (T*)(wsb + align16(sizeof(int) * (D.max_points + 1)));
+  double* costs = O.costs + (size_t)b * (max_it + 1);
+  double* lambdas = O.lambdas + (size_t)b * max_it;
+  uint8_t* accepted = O.accepted + (size_t)b * max_it;
+  uint8_t* evals = O.evals + (size_t)b * max_it;
+
+  // ---------------- setup ----------------
+  for (int i = tid; i < n * 9; i += NT) Rc[i] = O.R_in[cb * 9 + i];
+  for (int i = tid; i < n * 3; i += NT) tc[i] = O.t_in[cb * 3 + i];
+  if (O.points_in != O.points_out)
+    for (int i = tid; i < Pn * 3; i += NT) X[i] = O.points_in[pb * 3 + i];
+  int nf = 0;
+  {
+    unsigned fm = 0;
+    for (int c = 0; c < n; ++c) fm |= (D.fixed[cb + c] ? 0u : 1u) << c;  // n <= MAXC <= 32
+    nf = __popc(fm);
+    for (int c = tid; c < n; c += NT) slot[c] = ((fm >> c) & 1u) ? __popc(fm & ((1u << c) - 1u)) : -1;
+  }
+  const int C = 6 * nf + (has_f ? 1 : 0), FI = C - 1, CA = C * (C + 3) / 2;
+  if (tid == 0) s_flag = 0;
+  for (int p = tid; p <= Pn; p += NT) {
+    int a = 0, z = K;
+    while (a < z) {
+      const int mid = (a + z) >> 1;
+      if (__ldg(&obs[mid].pt) < p) a = mid + 1; else z = mid;
+    }
+    ptr[p] = a;
+  }
+  for (int j = tid; j < C; j += NT) {
+    const int a0 = acol(j, C);
+    for (int i = j; i <= C; ++i) tab[a0 + i - j] = (unsigned short)((i << 8) | j);
+  }
+  __syncthreads();
+  for (int k = tid; k < K; k += NT) {
+    const int pt = __ldg(&obs[k].pt), c = __ldg(&obs[k].cam);
+    const bool bad = pt < 0 || pt >= Pn || c < 0 || c >= n || (k > 0 && __ldg(&obs[k - 1].pt) > pt);
+    if (bad) s_flag = 1;
+  }
+  for (int p = tid; p < Pn; p += NT)
+    if (ptr[p + 1] - ptr[p] > kChunk) s_flag = 1;   // (host routes such batches elsewhere)
+  __syncthreads();
+  double f = O.focal_in[b];
+  if (s_flag) {
+    if (tid == 0) {
+      O.n_iters[b] = 0;
+      O.status[b] = -1;
+      O.focal_out[b] = f;
+    }
+    for (int i = tid; i < n * 9; i += NT) O.R_out[cb * 9 + i] = Rc[i];
+    for (int i = tid; i < n * 3; i += NT) O.t_out[cb * 3 + i] = tc[i];
+    __syncthreads();
+    return;
+  }
+  // this warp's contiguous point range
+  const int wp0 = (int)((int64_t)Pn * wid / NW), wp1 = (int)((int64_t)Pn * (wid + 1) / NW);
+
+  double stt[3];
+  {
+    // initial cost: block-wide pass
+    double acc3[3] = {0.0, 0.0, 0.0};
+    for (int k = tid; k < K; k += NT) {
+      Obs o = load_obs(obs, lo, k);
+      const double Xp[3] = {X[3 * o.pt], X[3 * o.pt + 1], X[3 * o.pt + 2]};
+      Proj pr = project_residual_fast(Rc + 9 * o.cam, tc + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
+      const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
+      acc3[0] += robust_rho(e, delta, loss);
+      acc3[1] += e;
+      acc3[2] += e * e;
+    }
+    block_sum<double, 3>(acc3, red);
+    stt[0] = acc3[0]; stt[1] = acc3[1]; stt[2] = acc3[2];
+  }
+  double cost = stt[0], se = stt[1], se2 = stt[2];
+  double lam = cfg.lambda_init;
+  if (tid == 0) costs[0] = cost;
+  int it = 0, stop_reason = MBA_SOLVE_MAX_ITERS;
+
+  for (; it < max_it;) {
+    const T tlam = T(lam);
+    for (int e = lane; e < CA; e += 32) Sw[e] = T(0);
+    for (int e = lane; e < C; e += 32) Ud[e] = T(0);
+    T part[4] = {T(0), T(0), T(0), T(0)};  // U_ff, g_f, sum yf.yf, sum yf.z
+    __syncwarp();
+    // ---------- per-warp point chunks ----------
+    for (int pc0 = wp0; pc0 < wp1;) {
+      // chunk: points [pc0, pc1) with at most kChunk observations
+      const int kc0 = ptr[pc0];
+      int pc1 = pc0 + 1;
+      while (pc1 < wp1 && pc1 - pc0 < kChunk && ptr[pc1 + 1] - kc0 <= kChunk) ++pc1;
+      const int kc1 = ptr[pc1];
+      const int npt = pc1 - pc0, nob = kc1 - kc0;
+      // (a) lane per observation
+      if (lane < nob) {
+        const int k = kc0 + lane;
+        Obs o = load_obs(obs, lo, k);
+        const double Xp[3] = {X[3 * o.pt], X[3 * o.pt + 1], X[3 * o.pt + 2]};
+        const double* Rk = Rc + 9 * o.cam;
+        Proj pr = project_residual_fast(Rk, tc + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
+        const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
+        const T w = T(robust_w(e, delta, loss));
+        T A[12], Fb[2], Bm[6];
+        jac_blocks<T>(pr, Rk, f, A, Fb, Bm);
+        const T r0 = T(pr.ru), r1 = T(pr.rv);
+        T* sr = st + lane * kSRow;
+#pragma unroll
+        for (int i = 0; i < 12; ++i) sr[i] = A[i];
+        sr[12] = Fb[0]; sr[13] = Fb[1]; sr[14] = r0; sr[15] = r1; sr[16] = w;
+        const int sl = slot[o.cam];
+        sslot[lane] = sl;
+        if (opt_pts) {
+          T wB[6];
+#pragma unroll
+          for (int i = 0; i < 6; ++i) wB[i] = w * Bm[i];
+          sr[35] = Bm[0] * wB[0] + Bm[3] * wB[3];
+          sr[36] = Bm[1] * wB[0] + Bm[4] * wB[3];
+          sr[37] = Bm[1] * wB[1] + Bm[4] * wB[4];
+          sr[38] = Bm[2] * wB[0] + Bm[5] * wB[3];
+          sr[39] = Bm[2] * wB[1] + Bm[5] * wB[4];
+          sr[40] = Bm[2] * wB[2] + Bm[5] * wB[5];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) sr[41 + a] = wB[a] * r0 + wB[3 + a] * r1;
+          const T wf0 = w * Fb[0], wf1 = w * Fb[1];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) sr[44 + a] = wf0 * Bm[a] + wf1 * Bm[3 + a];
+          if (sl >= 0) {
+#pragma unroll
+            for (int r = 0; r < 6; ++r)
+#pragma unroll
+              for (int a = 0; a < 3; ++a) sr[17 + r * 3 + a] = A[r] * wB[a] + A[6 + r] * wB[3 + a];
+          }
+        }
+      }
+      __syncwarp();
+      // (b) lane per point
+      if (lane < npt) {
+        const int p = pc0 + lane;
+        const int a0 = ptr[p] - kc0, a1 = ptr[p + 1] - kc0;
+        pi[2 * lane] = a0;
+        pi[2 * lane + 1] = a1;
+        T V[6] = {T(0), T(0), T(0), T(0), T(0), T(0)}, g[3] = {T(0), T(0), T(0)}, wf[3] = {T(0), T(0), T(0)};
+        for (int q = a0; q < a1; ++q) {
+          const T* sr = st + q * kSRow;
+          if (has_f) {
+            part[0] += sr[16] * (sr[12] * sr[12] + sr[13] * sr[13]);
+            part[1] += sr[16] * (sr[12] * sr[14] + sr[13] * sr[15]);
+          }
+          if (opt_pts) {
+#pragma unroll
+            for (int i = 0; i < 6; ++i) V[i] += sr[35 + i];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) g[i] += sr[41 + i];
+            if (has_f)
+#pragma unroll
+              for (int i = 0; i < 3; ++i) wf[i] += sr[44 + i];
+          }
+        }
+        if (opt_pts) {
+          V[0] += tlam * (V[0] > T(kDiagFloor) ? V[0] : T(kDiagFloor));
+          V[2] += tlam * (V[2] > T(kDiagFloor) ? V[2] : T(kDiagFloor));
+          V[5] += tlam * (V[5] > T(kDiagFloor) ? V[5] : T(kDiagFloor));
+          const T L00 = sqrt(V[0]);
+          const T i00 = T(1) / L00;
+          const T L10 = V[1] * i00, L20 = V[3] * i00;
+          const T L11 = sqrt(V[2] - L10 * L10);
+          const T i11 = T(1) / L11;
+          const T L21 = (V[4] - L20 * L10) * i11;
+          const T L22 = sqrt(V[5] - L20 * L20 - L21 * L21);
+          const T i22 = T(1) / L22;
+          const T z0 = g[0] * i00, z1 = (g[1] - L10 * z0) * i11, z2 = (g[2] - L20 * z0 - L21 * z1) * i22;
+          const T f0 = wf[0] * i00, f1 = (wf[1] - L10 * f0) * i11, f2 = (wf[2] - L20 * f0 - L21 * f1) * i22;
+          part[2] += f0 * f0 + f1 * f1 + f2 * f2;
+          part[3] += f0 * z0 + f1 * z1 + f2 * z2;
+          T* pl = ps + lane * 12;
+          pl[0] = L00; pl[1] = L10; pl[2] = L11; pl[3] = L20; pl[4] = L21; pl[5] = L22;
+          pl[6] = z0; pl[7] = z1; pl[8] = z2; pl[9] = f0; pl[10] = f1; pl[11] = f2;
+          T* pw = ptw + (size_t)p * 16;
+#pragma unroll
+          for (int i = 0; i < 12; ++i) pw[i] = pl[i];
+        }
+      }
+      __syncwarp();
+      if (opt_pts) {
+        // (c) lane per observation: Y_i = W_i L_p^-T
+        if (lane < nob && sslot[lane] >= 0) {
+          int lp = 0;
+          while (lp + 1 < npt && pi[2 * (lp + 1)] <= lane) ++lp;
+          const T* pl = ps + lp * 12;
+          const T L00 = pl[0], L10 = pl[1], L11 = pl[2], L20 = pl[3], L21 = pl[4], L22 = pl[5];
+          const T i00 = T(1) / L00, i11 = T(1) / L11, i22 = T(1) / L22;
+          T* y = st + lane * kSRow + 17;
+#pragma unroll
+          for (int r = 0; r < 6; ++r) {
+            const T y0 = y[r * 3 + 0] * i00;
+            const T y1 = (y[r * 3 + 1] - L10 * y0) * i11;
+            const T y2 = (y[r * 3 + 2] - L20 * y0 - L21 * y1) * i22;
+            y[r * 3 + 0] = y0;
+            y[r * 3 + 1] = y1;
+            y[r * 3 + 2] = y2;
+          }
+        }
+        __syncwarp();
+      }
+      // (d) point by point accumulation into the warp's S_aug
+      for (int lp = 0; lp < npt; ++lp) {
+        const int a0 = pi[2 * lp], a1 = pi[2 * lp + 1];
+        // free observations of the point (local staging indices), slot-ordered checks
+        int fre[kChunk];
+        int m = 0;
+        bool dup = false;
+        for (int q = a0; q < a1; ++q)
+          if (sslot[q] >= 0) {
+            for (int t = 0; t < m; ++t) dup |= sslot[fre[t]] == sslot[q];
+            fre[m++] = q;
+          }
+        const T* pl = ps + lp * 12;
+        if (opt_pts && !dup) {
+          // Schur 6x6 blocks: tasks (pair k >= l, row r)
+          const int ntask = 3 * m * (m + 1);
+          for (int tsk = lane; tsk < ntask; tsk += 32) {
+            const int pr_ = tsk / 6, r = tsk % 6;
+            int k = 0;
+            while ((k + 1) * (k + 2) / 2 <= pr_) ++k;
+            const int l = pr_ - k * (k + 1) / 2;
+            int qh = fre[k], ql = fre[l];
+            if (sslot[qh] < sslot[ql]) { const int tq = qh; qh = ql; ql = tq; }
+            const int sh = sslot[qh], sl_ = sslot[ql];
+            const T* yh = st + qh * kSRow + 17;
+            const T* yl = st + ql * kSRow + 17;
+            const T h0 = yh[r * 3], h1 = yh[r * 3 + 1], h2 = yh[r * 3 + 2];
+            const int row = 6 * sh + r;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+              if (sh == sl_ && c > r) continue;
+              const int col = 6 * sl_ + c;
+              Sw[acol(col, C) + row - col] -= h0 * yl[c * 3] + h1 * yl[c * 3 + 1] + h2 * yl[c * 3 + 2];
+            }
+          }
+          __syncwarp();
+        }
+        // rows of each free observation: J^T w J (camera block, focal, rhs) and
+        // the Schur focal / rhs terms
+        if (!dup) {
+          for (int tsk = lane; tsk < 6 * m; tsk += 32) {
+            const int kk = tsk / 6, r = tsk % 6;
+            const int q = fre[kk], s_ = sslot[q];
+            const T* sr = st + q * kSRow;
+            const T w = sr[16];
+            const T ar0 = w * sr[r], ar1 = w * sr[6 + r];
+            const int row = 6 * s_ + r;
+            const int cs = acol(row, C) - row;  // column `row`: entry (i, row) at cs + i
+            T d = T(0);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+              if (c > r) continue;
+              const T v = ar0 * sr[c] + ar1 * sr[6 + c];
+              if (c == r) d = v;
+              const int col = 6 * s_ + c;
+              Sw[acol(col, C) + row - col] += v;
+            }
+            Ud[row] += d;
+            T sf = T(0), sz = T(0);  // Schur focal / rhs terms (points optimised only)
+            if (opt_pts) {
+              const T yr0 = sr[17 + r * 3], yr1 = sr[18 + r * 3], yr2 = sr[19 + r * 3];
+              sf = yr0 * pl[9] + yr1 * pl[10] + yr2 * pl[11];
+              sz = yr0 * pl[6] + yr1 * pl[7] + yr2 * pl[8];
+            }
+            if (has_f) Sw[cs + FI] += ar0 * sr[12] + ar1 * sr[13] - sf;
+            Sw[cs + C] += -(ar0 * sr[14] + ar1 * sr[15]) + sz;
+          }
+          __syncwarp();
+        } else if (lane == 0) {
+          // duplicate camera within a point (rare): serial accumulation
+          for (int kk = 0; kk < m; ++kk) {
+            const int qk = fre[kk], sk = sslot[qk];
+            const T* srk = st + qk * kSRow;
+            for (int ll = 0; ll < m; ++ll) {
+              const int ql = fre[ll], sl2 = sslot[ql];
+              if (!opt_pts) break;
+              const T* yk = srk + 17;
+              const T* yl = st + ql * kSRow + 17;
+              for (int r = 0; r < 6; ++r)
+                for (int c = 0; c < 6; ++c) {
+                  const int row = 6 * sk + r, col = 6 * sl2 + c;
+                  if (row < col) continue;   // each ordered (row >= col) entry once per ordered pair
+                  Sw[acol(col, C) + row - col] -= yk[r * 3] * yl[c * 3] + yk[r * 3 + 1] * yl[c * 3 + 1] +
+                                                  yk[r * 3 + 2] * yl[c * 3 + 2];
+                }
+            }
+            const T w = srk[16];
+            for (int r = 0; r < 6; ++r) {
+              const int row = 6 * sk + r;
+              const int cs = acol(row, C) - row;
+              const T ar0 = w * srk[r], ar1 = w * srk[6 + r];
+              for (int c = 0; c <= r; ++c) {
+                const T v = ar0 * srk[c] + ar1 * srk[6 + c];
+                const int col = 6 * sk + c;
+                Sw[acol(col, C) + row - col] += v;
+                if (c == r) Ud[row] += v;
+              }
+              T sf = T(0), sz = T(0);
+              if (opt_pts) {
+                const T yr0 = srk[17 + r * 3], yr1 = srk[18 + r * 3], yr2 = srk[19 + r * 3];
+                sf = yr0 * pl[9] + yr1 * pl[10] + yr2 * pl[11];
+                sz = yr0 * pl[6] + yr1 * pl[7] + yr2 * pl[8];
+              }
+              if (has_f) Sw[cs + FI] += ar0 * srk[12] + ar1 * srk[13] - sf;
+              Sw[cs + C] += -(ar0 * srk[14] + ar1 * srk[15]) + sz;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      pc0 = pc1;
+    }
+    // ---------- combine the warps' systems ----------
+#pragma unroll
+    for (int i = 0; i < 4; ++i) part[i] = warp_sum(part[i]);
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ((T*)red)[wid * 4 + i] = part[i];
+    __syncthreads();
+    for (int e = tid; e < CA; e += NT) {
+      T v = T(0);
+      for (int w2 = 0; w2 < NW; ++w2) v += ((T*)(smem_raw + L::oSw))[(size_t)w2 * L::CA + e];
+      S[e] = v;
+    }
+    __syncthreads();
+    if (tid < C) {
+      const int g = tid;
+      T u = T(0);
+      for (int w2 = 0; w2 < NW; ++w2) u += ((T*)(smem_raw + L::oUd))[(size_t)w2 * L::C + g];
+      T pf[4] = {T(0), T(0), T(0), T(0)};
+      for (int w2 = 0; w2 < NW; ++w2)
+        for (int i = 0; i < 4; ++i) pf[i] += ((T*)red)[w2 * 4 + i];
+      if (has_f && g == FI) {
+        const T uff = pf[0];
+        S[acol(FI, C)] = uff + tlam * (uff > T(kDiagFloor) ? uff : T(kDiagFloor)) - pf[2];
+        S[acol(FI, C) + 1] = -pf[1] + pf[3];
+      } else {
+        S[acol(g, C)] += tlam * (u > T(kDiagFloor) ? u : T(kDiagFloor));
+      }
+    }
+    __syncthreads();
+
+    // ---------- LDL^T (forward substitution fused) ----------
+    bool chol_fail = false;
+    for (int k = 0; k < C; ++k) {
+      const T* colk = S + acol(k, C) - k;
+      const T d = colk[k];
+      if (!(d > T(0)) || !isfinite((double)d)) {
+        chol_fail = true;
+        break;
+      }
+      const T inv = T(1) / d;
+      for (int e = acol(k + 1, C) + tid; e < CA; e += NT) {
+        const unsigned ij = tab[e];
+        S[e] -= colk[ij >> 8] * colk[ij & 255u] * inv;
+      }
+      __syncthreads();
+    }
+    if (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull)) chol_fail = true;
+
+    if (!chol_fail) {
+      if (wid == 0) {
+        for (int k = C - 1; k >= 0; --k) {
+          const T* colk = S + acol(k, C) - k;
+          T acc = T(0);
+          for (int i = k + 1 + lane; i < C; i += 32) acc += colk[i] * xs[i];
+          acc = warp_sum(acc);
+          const T xk = (colk[C] - acc) / colk[k];
+          if (lane == 0) xs[k] = xk;
+          __syncwarp();
+        }
+        for (int i = lane; i < C; i += 32) dcs[i] = (double)xs[i];
+      }
+      __syncthreads();
+      // point back-substitution, recomputing W_i^T dc = w B^T (A dc)
+      if (opt_pts) {
+        const T df = has_f ? T(dcs[FI]) : T(0);
+        for (int p = tid; p < Pn; p += NT) {
+          const double Xp[3] = {X[3 * p], X[3 * p + 1], X[3 * p + 2]};
+          T u0 = T(0), u1 = T(0), u2 = T(0);
+          for (int k = ptr[p]; k < ptr[p + 1]; ++k) {
+            Obs o = load_obs(obs, lo, k);
+            const int s_ = slot[o.cam];
+            if (s_ < 0) continue;
+            const double* Rk = Rc + 9 * o.cam;
+            Proj pr = project_residual_fast(Rk, tc + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
+            const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
+            const T w = T(robust_w(e, delta, loss));
+            T A[12], Fb[2], Bm[6];
+            jac_blocks<T>(pr, Rk, f, A, Fb, Bm);
+            T ad0 = T(0), ad1 = T(0);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+              const T dd = T(dcs[6 * s_ + c]);
+              ad0 += A[c] * dd;
+              ad1 += A[6 + c] * dd;
+            }
+            ad0 *= w;
+            ad1 *= w;
+            u0 += Bm[0] * ad0 + Bm[3] * ad1;
+            u1 += Bm[1] * ad0 + Bm[4] * ad1;
+            u2 += Bm[2] * ad0 + Bm[5] * ad1;
+          }
+          T* pw = ptw + (size_t)p * 16;
+          const T L00 = pw[0], L10 = pw[1], L11 = pw[2], L20 = pw[3], L21 = pw[4], L22 = pw[5];
+          // v = L^-1 (W^T dc), then dp = -L^-T (z + v + yf df)
+          const T v0 = u0 / L00, v1 = (u1 - L10 * v0) / L11, v2 = (u2 - L20 * v0 - L21 * v1) / L22;
+          const T t0 = pw[6] + v0 + pw[9] * df, t1 = pw[7] + v1 + pw[10] * df, t2 = pw[8] + v2 + pw[11] * df;
+          const T x2 = t2 / L22;
+          const T x1 = (t1 - L21 * x2) / L11;
+          const T x0 = (t0 - L10 * x1 - L20 * x2) / L00;
+          pw[12] = -x0;
+          pw[13] = -x1;
+          pw[14] = -x2;
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---------- trials ----------
+    if (tid == 0) lambdas[it] = lam;
+    int tries = 0, took = -1;
+    double tcst[3] = {0, 0, 0};
+    double ft = f;
+    if (!chol_fail) {
+      for (int q = tid; q < kBacktrackTries * n; q += NT) {
+        const int bt = q / n, c = q % n, s_ = slot[c];
+        const double frac = ldexp(1.0, -bt);
+        double* Rq = Rt + (size_t)(bt * n + c) * 9;
+        double* tq = tt + (size_t)(bt * n + c) * 3;
+        if (s_ < 0) {
+          for (int i = 0; i < 9; ++i) Rq[i] = Rc[9 * c + i];
+          for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i];
+        } else {
+          const double w[3] = {frac * dcs[6 * s_], frac * dcs[6 * s_ + 1], frac * dcs[6 * s_ + 2]};
+          double E[9];
+          exp_so3(w, E);
+          matmul33(E, Rc + 9 * c, Rq);
+          for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i] + frac * dcs[6 * s_ + 3 + i];
+        }
+      }
+      __syncthreads();
+      for (int bt = 0; bt < kBacktrackTries; ++bt) {
+        const double frac = ldexp(1.0, -bt);
+        ft = has_f ? f + frac * dcs[FI] : f;
+        const double* Rs = Rt + (size_t)bt * n * 9;
+        const double* ts = tt + (size_t)bt * n * 3;
+        double acc3[3] = {0.0, 0.0, 0.0};
+        for (int k0 = tid; k0 < K; k0 += 4 * NT) {
+          Obs o[4];
+          double Xq[4][3];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (k0 + u * NT < K) o[u] = load_obs(obs, lo, k0 + u * NT);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (k0 + u * NT >= K) continue;
+            const double* x = X + 3 * o[u].pt;
+            Xq[u][0] = x[0]; Xq[u][1] = x[1]; Xq[u][2] = x[2];
+            if (opt_pts) {
+              const T* dp = ptw + (size_t)o[u].pt * 16 + 12;
+              Xq[u][0] = Xq[u][0] + frac * (double)dp[0];
+              Xq[u][1] = Xq[u][1] + frac * (double)dp[1];
+              Xq[u][2] = Xq[u][2] + frac * (double)dp[2];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (k0 + u * NT >= K) continue;
+            Proj pr = project_residual_fast(Rs + 9 * o[u].cam, ts + 3 * o[u].cam, Xq[u], ft, cx, cy, o[u].u, o[u].v);
+            const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
+            acc3[0] += robust_rho(e, delta, loss);
+            acc3[1] += e;
+            acc3[2] += e * e;
+          }
+        }
+        block_sum<double, 3>(acc3, red);
+        tcst[0] = acc3[0]; tcst[1] = acc3[1]; tcst[2] = acc3[2];
+        ++tries;
+        if (tcst[0] < cost && isfinite(tcst[0])) {
+          took = bt;
+          break;
+        }
+      }
+    }
+    if (tid == 0) evals[it] = (uint8_t)tries;
+    bool stop = false;
+    if (took >= 0) {
+      const double frac = ldexp(1.0, -took);
+      for (int i = tid; i < n * 9; i += NT) Rc[i] = Rt[(size_t)took * n * 9 + i];
+      for (int i = tid; i < n * 3; i += NT) tc[i] = tt[(size_t)took * n * 3 + i];
+      if (opt_pts)
+        for (int p = tid; p < Pn; p += NT) {
+          const T* dp = ptw + (size_t)p * 16 + 12;
+          X[3 * p + 0] = X[3 * p + 0] + frac * (double)dp[0];
+          X[3 * p + 1] = X[3 * p + 1] + frac * (double)dp[1];
+          X[3 * p + 2] = X[3 * p + 2] + frac * (double)dp[2];
+        }
+      f = ft;
+      lam = took == 0 ? fmax(lam / nu, 1e-15) : fmin(lam * nu, kLambdaMax);
+      const double improve = cost - tcst[0];
+      cost = tcst[0];
+      se = tcst[1];
+      se2 = tcst[2];
+      if (tid == 0) accepted[it] = 1;
+      if (improve <= 1e-15 * fmax(cost, 1.0)) {
+        stop = true;
+        stop_reason = MBA_SOLVE_CONVERGED;
+      }
+    } else {
+      lam = fmin(lam * nu, kLambdaMax);
+      if (tid == 0) accepted[it] = 0;
+      if (!chol_fail && lam >= kLambdaMax) {
+        stop = true;
+        stop_reason = MBA_SOLVE_LAMBDA_CAP;
+      }
+    }
+    if (tid == 0) costs[it + 1] = cost;
+    ++it;
+    __syncthreads();
+    if (stop) break;
+  }
+
+  for (int i = tid; i < n * 9; i += NT) O.R_out[cb * 9 + i] = Rc[i];
+  for (int i = tid; i < n * 3; i += NT) O.t_out[cb * 3 + i] = tc[i];
+  if (tid == 0) {
+    O.focal_out[b] = f;
+    O.n_iters[b] = it;
+    O.status[b] = stop_reason;
+    O.final_stats[4 * b + 0] = cost;
+    O.final_stats[4 * b + 1] = se;
+    O.final_stats[4 * b + 2] = se2;
+    O.final_stats[4 * b + 3] = (double)K;
+  }
+  __syncthreads();
+}
+
+template <typename T, int MAXC, int NW>
+__global__ void __launch_bounds__(32 * NW) solve_pw_kernel(SolveParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_prob;
+  for (;;) {
+    if (threadIdx.x == 0) s_prob = atomicAdd(P.counter, 1);
+    __syncthreads();
+    const int b = s_prob;
+    __syncthreads();
+    if (b >= P.d.n_problems) return;
+    pw_solve_one<T, MAXC, NW>(P, b, smem_raw);
+  }
+}
+
+template <typename T, int MAXC, int NW>
+static int launch_pw(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t scratch = pw_scratch_bytes<T>(d->max_points);
+  const size_t smem = PLayout<T, MAXC, NW>::kBytes;
+  if (smem > 227 * 1024) return MBA_ERR_TOO_LARGE;
+  cudaFuncSetAttribute(solve_pw_kernel<T, MAXC, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_pw_kernel<T, MAXC, NW>, 32 * NW, smem);
+  if (per_sm < 1) return MBA_ERR_TOO_LARGE;
+  int grid = n_sm * per_sm;
+  if (grid > d->n_problems) grid = d->n_problems;
+  if (ws_bytes < 256 + scratch * (size_t)grid) return MBA_ERR_INVALID;
+  SolveParams P;
+  P.d = *d;
+  P.cfg = *cfg;
+  P.o = *o;
+  P.counter = (int*)ws;
+  P.ws = (unsigned char*)ws + 256;
+  P.ws_slot_bytes = scratch;
+  P.max_cams = d->max_cams;
+  cudaMemsetAsync(ws, 0, sizeof(int), st);
+  solve_pw_kernel<T, MAXC, NW><<<grid, 32 * NW, smem, st>>>(P);
+  return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
+}
+
 constexpr size_t kSmemLimit = 227 * 1024;
 
 template <typename T, int MAXC, bool RES>
@@ -1541,15 +2217,20 @@ static int launch_warp(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaO
 // Kernel choice: many small problems -> one warp per problem; otherwise one
 // CTA per problem (scratch in shared memory when it fits).
 static int choose_mode(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
-  if (cfg->ctas_per_problem < 0) return -cfg->ctas_per_problem;   // forced (tests): 1 = warp, 2 = CTA
+  if (cfg->ctas_per_problem < 0) return -cfg->ctas_per_problem;   // forced: 1 warp, 2 CTA, 3 point-wise
+  // measured on config 4: CTA-resident 133k problems/s, point-wise
+  // 73k, warp-per-problem 72k (mixed) -> the CTA kernel is the default
   (void)d;
-  return 2;  // the CTA kernel measured faster on every BASELINE config
+  return 2;
 }
 
 template <typename T>
 static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
-  if (d->max_cams <= 8 && choose_mode(d, cfg) == 1) return launch_warp<T, 8>(d, cfg, o, ws, ws_bytes, st);
+  const int mode = choose_mode(d, cfg);
+  if (d->max_cams <= 8 && d->max_track <= kChunk && mode == 3)
+    return launch_pw<T, 8, sizeof(T) == 4 ? 4 : 2>(d, cfg, o, ws, ws_bytes, st);
+  if (d->max_cams <= 8 && mode == 1) return launch_warp<T, 8>(d, cfg, o, ws, ws_bytes, st);
   if (d->max_cams <= 8) {
     if (resident_fits<T, 8>(d)) return launch_cfg<T, 8, true>(d, cfg, o, ws, ws_bytes, st);
     return launch_cfg<T, 8, false>(d, cfg, o, ws, ws_bytes, st);

@@ -35,6 +35,7 @@ class HostBatch:
     focal: np.ndarray
     points: np.ndarray
     max_pairs: int = 0
+    max_track: int = 0
 
     @property
     def n_problems(self):
@@ -53,14 +54,17 @@ class HostBatch:
         return int(np.max(np.diff(self.pt_off))) if self.n_problems else 0
 
 
-def _max_pairs(obs_off, pt_off, pt):
-    """max over problems of sum_p m_p (m_p + 1) / 2 (co-observation pairs)."""
+def _track_stats(obs_off, pt_off, pt):
+    """(max over problems of sum_p m_p (m_p + 1) / 2, max m_p), m_p = observations of point p."""
     n_obs = np.diff(obs_off)
     gpt = np.repeat(pt_off[:-1], n_obs) + pt
     m = np.bincount(gpt, minlength=int(pt_off[-1])).astype(np.int64)
     per_pt = m * (m + 1) // 2
     prob = np.repeat(np.arange(len(n_obs)), np.diff(pt_off))
-    return int(np.bincount(prob, weights=per_pt, minlength=len(n_obs)).max()) if len(n_obs) else 0
+    if not len(n_obs):
+        return 0, 0
+    return (int(np.bincount(prob, weights=per_pt, minlength=len(n_obs)).max()),
+            int(m.max()) if len(m) else 0)
 
 
 def _records(uv, cam, pt):
@@ -117,7 +121,8 @@ def pack_problems(problems) -> HostBatch:
                      cx=np.array(cx), cy=np.array(cy), flags=np.array(fl, dtype=np.uint8),
                      R=np.concatenate(Rs), t=np.concatenate(ts), focal=np.array(foc),
                      points=np.concatenate(pts),
-                     max_pairs=_max_pairs(obs_off, pt_off, obs.view(np.int32)[:, 3]))
+                     **dict(zip(("max_pairs", "max_track"),
+                                _track_stats(obs_off, pt_off, obs.view(np.int32)[:, 3]))))
 
 
 def pack_synth(b) -> HostBatch:
@@ -128,7 +133,7 @@ def pack_synth(b) -> HostBatch:
     return HostBatch(cam_off=b.cam_off, pt_off=b.pt_off, obs_off=b.obs_off, obs=rec,
                      obs_lo=lo if np.any(lo) else None, fixed=b.fixed.astype(np.uint8), cx=b.cx,
                      cy=b.cy, flags=flags, R=b.R, t=b.t, focal=b.focal, points=b.points,
-                     max_pairs=_max_pairs(b.obs_off, b.pt_off, b.pt))
+                     **dict(zip(("max_pairs", "max_track"), _track_stats(b.obs_off, b.pt_off, b.pt))))
 
 
 @dataclass
@@ -138,6 +143,7 @@ class DeviceBatch:
     max_obs: int
     max_points: int
     max_pairs: int
+    max_track: int
     cam_off: object
     pt_off: object
     obs_off: object
@@ -184,7 +190,8 @@ def to_device(hb: HostBatch, device=None, pinned=None) -> DeviceBatch:
         d[k] = a.to(dev, non_blocking=True)
         nbytes += a.numel() * a.element_size()
     return DeviceBatch(n_problems=hb.n_problems, max_cams=hb.max_cams, max_obs=hb.max_obs,
-                       max_points=hb.max_points, max_pairs=hb.max_pairs, h2d_bytes=nbytes, **d)
+                       max_points=hb.max_points, max_pairs=hb.max_pairs, max_track=hb.max_track,
+                       h2d_bytes=nbytes, **d)
 
 
 @dataclass
@@ -196,7 +203,7 @@ class LmParams:
     loss: str = "huber"
     precision: str = "f64"
     fail_at: tuple = ()
-    kernel: str = "auto"      # "auto" | "warp" (one warp per problem) | "cta" (one CTA per problem)
+    kernel: str = "auto"      # "auto" | "pw" (point-wise) | "warp" (warp per problem) | "cta" (CTA per problem)
 
     @staticmethod
     def from_cfg(cfg, **over):
@@ -248,13 +255,13 @@ def _workspace(nbytes, device):
 
 def descriptors(db: DeviceBatch, prm: LmParams, sol: Solution):
     d = MbaBatchDesc(n_problems=db.n_problems, max_cams=db.max_cams, max_obs=db.max_obs,
-                     max_points=db.max_points, max_pairs=db.max_pairs, cam_off=ptr(db.cam_off), pt_off=ptr(db.pt_off),
+                     max_points=db.max_points, max_pairs=db.max_pairs, max_track=db.max_track, cam_off=ptr(db.cam_off), pt_off=ptr(db.pt_off),
                      obs_off=ptr(db.obs_off), obs=ptr(db.obs), obs_lo=ptr(db.obs_lo),
                      fixed=ptr(db.fixed), cx=ptr(db.cx), cy=ptr(db.cy), flags=ptr(db.flags))
     c = MbaLmConfig(lambda_init=prm.lambda_init, nu=prm.nu, delta=prm.delta,
                     max_iters=prm.max_iters, loss=_lib.LOSS[prm.loss],
                     precision=_lib.PRECISION[prm.precision],
-                    ctas_per_problem={"auto": 0, "warp": -1, "cta": -2}[prm.kernel],
+                    ctas_per_problem={"auto": 0, "warp": -1, "cta": -2, "pw": -3}[prm.kernel],
                     fail_iters_mask=sum(1 << int(i) for i in prm.fail_at if 0 <= int(i) < 64))
     o = MbaOutputs(R_in=ptr(db.R), t_in=ptr(db.t), focal_in=ptr(db.focal), points_in=ptr(db.points),
                    R_out=ptr(sol.R), t_out=ptr(sol.t), focal_out=ptr(sol.focal),

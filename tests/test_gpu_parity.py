@@ -12,7 +12,7 @@ from oracle import miniba_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp"])
+@pytest.mark.parametrize("kernel", ["cta", "warp", "pw"])
 @pytest.mark.parametrize("path", golden_cases(), ids=golden_ids())
 def test_solver_matches_reference_golden(path, kernel, cuda_ok):
     """float64 mode (the API default): exact trace parity through i* (fp64
@@ -63,7 +63,7 @@ def test_mixed_precision_against_golden(path, cuda_ok):
         assert np.abs(t - out["t"]).max() <= 1e-3 * scale
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp"])
+@pytest.mark.parametrize("kernel", ["cta", "warp", "pw"])
 @pytest.mark.parametrize("precision", ["mixed", "f64"])
 def test_batched_matches_oracle_and_is_shard_invariant(precision, kernel, cuda_ok):
     from paper_2506_05558_b200.synth import make_batch
@@ -122,7 +122,7 @@ def test_cauchy_outliers_many_cameras(cuda_ok):
                   p["focal"], label="cauchy16")
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp"])
+@pytest.mark.parametrize("kernel", ["cta", "warp", "pw"])
 def test_fault_injection_matches_oracle(kernel, cuda_ok):
     from paper_2506_05558_b200.synth import make_batch
     p = make_batch(1, n_cams=8, K=2000, seed=4).problem(0)
@@ -147,7 +147,7 @@ def test_max_iters_zero_and_one(cuda_ok):
     np.testing.assert_allclose(d1["costs"], ref["costs"], rtol=1e-9)
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp"])
+@pytest.mark.parametrize("kernel", ["cta", "warp", "pw"])
 def test_all_cameras_fixed_focal_only(kernel, cuda_ok):
     """C = 1 (focal only) edge shape."""
     from paper_2506_05558_b200.synth import make_batch
@@ -159,14 +159,14 @@ def test_all_cameras_fixed_focal_only(kernel, cuda_ok):
     assert dev["accepted"][:3].tolist() == ref["accepted"][:3].tolist()
 
 
-def test_warp_and_cta_kernels_agree(cuda_ok):
-    """Both kernels implement the same arithmetic in the same order per
-    problem except reduction trees: traces agree through i* and final costs
-    to 1e-9 on a 64-problem batch."""
+@pytest.mark.parametrize("other", ["warp", "pw"])
+def test_kernels_agree(other, cuda_ok):
+    """All kernels implement the same arithmetic per problem up to reduction
+    order: traces agree through i* and final costs to 1e-9 on 64 problems."""
     from paper_2506_05558_b200.synth import make_batch
     b = make_batch(64, n_cams=8, K=2000, seed=21)
     probs = [b.problem(i) for i in range(64)]
-    w = run_device(probs, dict(max_iters=200), "f64", "warp")
+    w = run_device(probs, dict(max_iters=200), "f64", other)
     c = run_device(probs, dict(max_iters=200), "f64", "cta")
     for x, y in zip(w, c):
         i_star = O.plateau_index(y["costs"])
