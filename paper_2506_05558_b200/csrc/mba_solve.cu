@@ -40,6 +40,8 @@
 
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "mba_common.cuh"
 
 namespace mba {
@@ -74,6 +76,7 @@ struct SolveParams {
   unsigned char* ws;       // per-slot workspace base
   size_t ws_slot_bytes;
   int max_cams;
+  unsigned char* grid;     // cooperative (multi-CTA) mode: cross-CTA buffers
 };
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -208,20 +211,21 @@ template <typename T>
 __device__ void cost_pass(const MbaObs* __restrict__ obs, const float* __restrict__ lo, int K,
                           const double* __restrict__ X, const T* __restrict__ ptw, double frac,
                           bool use_dp, const double* Rs, const double* ts, double f, double cx,
-                          double cy, double delta, int loss, double* red, double out[3]) {
+                          double cy, double delta, int loss, double* red, double out[3],
+                          int start, int stride) {
   constexpr int U = 4;
   double acc[3] = {0.0, 0.0, 0.0};
-  for (int k0 = threadIdx.x; k0 < K; k0 += U * blockDim.x) {
+  for (int k0 = start; k0 < K; k0 += U * stride) {
     Obs o[U];
     double Xp[U][3];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int k = k0 + u * blockDim.x;
+      const int k = k0 + u * stride;
       if (k < K) o[u] = load_obs(obs, lo, k);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int k = k0 + u * blockDim.x;
+      const int k = k0 + u * stride;
       if (k >= K) continue;
       const double* x = X + 3 * o[u].pt;
       Xp[u][0] = x[0];
@@ -236,7 +240,7 @@ __device__ void cost_pass(const MbaObs* __restrict__ obs, const float* __restric
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int k = k0 + u * blockDim.x;
+      const int k = k0 + u * stride;
       if (k >= K) continue;
       Proj pr = project_residual_fast(Rs + 9 * o[u].cam, ts + 3 * o[u].cam, Xp[u], f, cx, cy, o[u].u, o[u].v);
       double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
@@ -294,10 +298,47 @@ __device__ __forceinline__ Scratch<T, RES> scratch_at(unsigned char* base, const
   return w;
 }
 
-template <typename T, int MAXC, bool RES>
+// Cross-CTA buffers of the cooperative mode (one problem spread over the grid).
+template <typename T, int MAXC>
+struct GridBufs {
+  static constexpr int C = 6 * MAXC + 1, CA = C * (C + 3) / 2, NB = MAXC * (MAXC + 1) / 2;
+  static constexpr size_t oS = 0;                                     // T[CA]
+  static constexpr size_t oU = align16(oS + sizeof(T) * CA);          // T[MAXC][kUcamStride]
+  static constexpr size_t oCnt = align16(oU + sizeof(T) * MAXC * kUcamStride);  // int[MAXC + NB + 2]
+  static constexpr size_t oRed = align16(oCnt + 4 * (MAXC + NB + 2)); // double[2][G][4]
+  static __host__ __device__ size_t bytes(int G) { return oRed + 8 * 2 * 4 * (size_t)G; }
+};
+
+template <typename T, int MAXC, bool RES, bool GRID = false>
 __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) {
   using L = Layout<T, MAXC>;
+  using GB = GridBufs<T, MAXC>;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // work distribution: one CTA (batched mode) or the whole grid (cooperative mode)
+  const int rank = GRID ? (int)blockIdx.x : 0, nranks = GRID ? (int)gridDim.x : 1;
+  const int gtid = rank * blockDim.x + tid, gthreads = nranks * blockDim.x;
+  const int gwid = rank * kWarps + wid, gwarps = nranks * kWarps;
+  const bool lead = tid == 0 && rank == 0;    // writes traces and outputs
+  auto gsync = [&]() {
+    if constexpr (GRID) cooperative_groups::this_grid().sync();
+    else __syncthreads();
+  };
+  int red_epoch = 0;
+  // deterministic cross-CTA sum of N per-CTA values (after a block_sum)
+  auto grid_sum = [&](double* v, int N) {
+    if constexpr (GRID) {
+      double* buf = (double*)(P.grid + GB::oRed) + (size_t)(red_epoch & 1) * nranks * 4;
+      ++red_epoch;
+      if (tid == 0)
+        for (int i = 0; i < N; ++i) buf[rank * 4 + i] = v[i];
+      gsync();
+      for (int i = 0; i < N; ++i) {
+        double s_ = 0.0;
+        for (int r = 0; r < nranks; ++r) s_ += buf[r * 4 + i];
+        v[i] = s_;
+      }
+    }
+  };
   const MbaBatchDesc& D = P.d;
   const MbaLmConfig& cfg = P.cfg;
   const MbaOutputs& O = P.o;
@@ -342,7 +383,8 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   double* __restrict__ X = O.points_out + 3 * pb;
 
   const Scratch<T, RES> W = scratch_at<T, RES>(
-      RES ? smem_raw + L::kFixed : P.ws + (size_t)blockIdx.x * P.ws_slot_bytes, D);
+      RES ? smem_raw + L::kFixed : P.ws + (GRID ? 0 : (size_t)blockIdx.x * P.ws_slot_bytes), D);
+  int* gcnt = GRID ? (int*)(P.grid + GB::oCnt) : nullptr;
   constexpr int YSTR = YS<RES>::v;
   auto ld18 = [](const T* p, T y[18]) {
     if constexpr (RES && sizeof(T) == 4) load18v2((const float*)p, (float*)y); else load18(p, y);
@@ -365,7 +407,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   for (int i = tid; i < n * 9; i += blockDim.x) sm.Rc[i] = O.R_in[cb * 9 + i];
   for (int i = tid; i < n * 3; i += blockDim.x) sm.tc[i] = O.t_in[cb * 3 + i];
   if (O.points_in != O.points_out)
-    for (int i = tid; i < Pn * 3; i += blockDim.x) X[i] = O.points_in[pb * 3 + i];
+    for (int i = gtid; i < Pn * 3; i += gthreads) X[i] = O.points_in[pb * 3 + i];
   if (tid == 0) {
     int nf = 0;
     for (int c = 0; c < n; ++c) {
@@ -388,7 +430,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     s_flag = 0;
   }
   // point CSR: observations are point-major; ptr[p] = first k with pt >= p
-  for (int p = tid; p <= Pn; p += blockDim.x) {
+  for (int p = gtid; p <= Pn; p += gthreads) {
     int lo_i = 0, hi_i = K;
     while (lo_i < hi_i) {
       int mid = (lo_i + hi_i) >> 1;
@@ -396,29 +438,37 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     }
     ptr[p] = lo_i;
   }
-  for (int k = tid; k < K; k += blockDim.x) {
+  for (int k = gtid; k < K; k += gthreads) {
     int pt = __ldg(&obs[k].pt), c = __ldg(&obs[k].cam);
     bool bad = pt < 0 || pt >= Pn || c < 0 || c >= n || (k > 0 && __ldg(&obs[k - 1].pt) > pt);
     if (bad) s_flag = 1;
   }
   __syncthreads();
+  if constexpr (GRID) {
+    double fv = s_flag;
+    __syncthreads();
+    grid_sum(&fv, 1);
+    if (tid == 0) s_flag = fv != 0.0;
+  }
   // camera-major permutation: warp per camera, two ballot sweeps
-  for (int c = wid; c < n; c += kWarps) {
+  for (int c = gwid; c < n; c += gwarps) {
     int cnt = 0;
     for (int k0 = 0; k0 < K; k0 += 32) {
       int k = k0 + lane;
       bool hit = k < K && obs_cam(obs, k) == c;
       cnt += __popc(__ballot_sync(0xffffffffu, hit));
     }
-    if (lane == 0) sm.cam_ptr[c + 1] = cnt;
+    if (lane == 0) {
+      if constexpr (GRID) gcnt[c + 1] = cnt; else sm.cam_ptr[c + 1] = cnt;
+    }
   }
-  __syncthreads();
+  gsync();
   if (tid == 0) {
     sm.cam_ptr[0] = 0;
-    for (int c = 0; c < n; ++c) sm.cam_ptr[c + 1] += sm.cam_ptr[c];
+    for (int c = 0; c < n; ++c) sm.cam_ptr[c + 1] = sm.cam_ptr[c] + (GRID ? gcnt[c + 1] : sm.cam_ptr[c + 1]);
   }
   __syncthreads();
-  for (int c = wid; c < n; c += kWarps) {
+  for (int c = gwid; c < n; c += gwarps) {
     int base = sm.cam_ptr[c];
     for (int k0 = 0; k0 < K; k0 += 32) {
       int k = k0 + lane;
@@ -428,12 +478,13 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       base += __popc(m);
     }
   }
-  __syncthreads();
+  gsync();
   const int nf = s_nf, C = s_C, FI = C - 1;
   const int nb = opt_pts ? nf * (nf + 1) / 2 : 0;
   // co-observation pair lists per camera block (a <= b): count, scan, fill
+  int* blk_cnt = GRID ? gcnt + MAXC + 1 : sm.blk_off;
   for (int pass = 0; pass < 2; ++pass) {
-    for (int blk = wid; blk < nb; blk += kWarps) {
+    for (int blk = gwid; blk < nb; blk += gwarps) {
       const int ca = sm.cam_of_slot[sm.blk_a[blk]], cbb = sm.cam_of_slot[sm.blk_b[blk]];
       const int q1 = sm.cam_ptr[ca + 1];
       int base = pass ? sm.blk_off[blk] : 0;
@@ -454,12 +505,12 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
         }
         base += warp_sum(m);
       }
-      if (!pass && lane == 0) sm.blk_off[blk + 1] = base;
+      if (!pass && lane == 0) blk_cnt[blk + 1] = base;
     }
-    __syncthreads();
+    gsync();
     if (!pass && tid == 0) {
       sm.blk_off[0] = 0;
-      for (int q = 0; q < nb; ++q) sm.blk_off[q + 1] += sm.blk_off[q];
+      for (int q = 0; q < nb; ++q) sm.blk_off[q + 1] = sm.blk_off[q] + blk_cnt[q + 1];
     }
     __syncthreads();
   }
@@ -471,13 +522,15 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   const int CA = C * (C + 3) / 2;
   double f = O.focal_in[b];
   if (s_flag) {  // malformed problem: report and leave parameters untouched
-    if (tid == 0) {
+    if (lead) {
       O.n_iters[b] = 0;
       O.status[b] = -1;
       if (O.focal_out) O.focal_out[b] = f;
     }
-    for (int i = tid; i < n * 9; i += blockDim.x) O.R_out[cb * 9 + i] = sm.Rc[i];
-    for (int i = tid; i < n * 3; i += blockDim.x) O.t_out[cb * 3 + i] = sm.tc[i];
+    if (rank == 0) {
+      for (int i = tid; i < n * 9; i += blockDim.x) O.R_out[cb * 9 + i] = sm.Rc[i];
+      for (int i = tid; i < n * 3; i += blockDim.x) O.t_out[cb * 3 + i] = sm.tc[i];
+    }
     __syncthreads();
     return;
   }
@@ -485,18 +538,20 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   PROF_MARK(PH_SETUP)
   // initial cost (miniba.py:232-235)
   double st[3];
-  cost_pass<T>(obs, lo, K, X, ptw, 0.0, false, sm.Rc, sm.tc, f, cx, cy, delta, loss, sm.red, st);
+  cost_pass<T>(obs, lo, K, X, ptw, 0.0, false, sm.Rc, sm.tc, f, cx, cy, delta, loss, sm.red, st,
+               gtid, gthreads);
+  grid_sum(st, 3);
   PROF_MARK(PH_COST0)
   double cost = st[0], se = st[1], se2 = st[2];
   double lam = cfg.lambda_init;
-  if (tid == 0) costs[0] = cost;
+  if (lead) costs[0] = cost;
   int it = 0, stop_reason = MBA_SOLVE_MAX_ITERS;
 
   for (; it < max_it;) {
     const T tlam = T(lam);
     // ---------- K1+K2 point pass ----------
     T part[4] = {T(0), T(0), T(0), T(0)};  // U_ff, g_f, sum yf.yf, sum yf.z
-    for (int p = tid; p < Pn; p += blockDim.x) {
+    for (int p = gtid; p < Pn; p += gthreads) {
       const double Xp[3] = {X[3 * p], X[3 * p + 1], X[3 * p + 2]};
       const int k0 = ptr[p], k1 = ptr[p + 1];
       T V[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};  // 00 10 11 20 21 22
@@ -582,13 +637,20 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     {
       T pf[4] = {part[0], part[1], part[2], part[3]};
       block_sum<T, 4>(pf, (T*)s_red4);
+      if constexpr (GRID) {
+        double pd[4] = {(double)pf[0], (double)pf[1], (double)pf[2], (double)pf[3]};
+        grid_sum(pd, 4);   // also the barrier that publishes Y / point factors
+        for (int i = 0; i < 4; ++i) pf[i] = T(pd[i]);
+      }
       part[0] = pf[0]; part[1] = pf[1]; part[2] = pf[2]; part[3] = pf[3];
     }
     // (block_sum ended with __syncthreads: point factors are visible)
     PROF_MARK(PH_POINT)
 
     // ---------- K2 camera jobs + K3 pair jobs (one warp per job) ----------
-    for (int job = wid; job < nf + nb; job += kWarps) {
+    T* S_jobs = GRID ? (T*)(P.grid + GB::oS) : sm.S;
+    T* U_jobs = GRID ? (T*)(P.grid + GB::oU) : sm.ucam;
+    for (int job = gwid; job < nf + nb; job += gwarps) {
       if (job < nf) {
         const int s = job, c = sm.cam_of_slot[s];
         const double* Rk = sm.Rc + 9 * c;
@@ -629,7 +691,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
 #pragma unroll
         for (int i = 0; i < kUcamStride; ++i) acc[i] = warp_sum(acc[i]);
         if (lane == 0)
-          for (int i = 0; i < kUcamStride; ++i) sm.ucam[s * kUcamStride + i] = acc[i];
+          for (int i = 0; i < kUcamStride; ++i) U_jobs[s * kUcamStride + i] = acc[i];
       } else {
         const int blk = job - nf;
         const int sa = sm.blk_a[blk], sb = sm.blk_b[blk];
@@ -658,15 +720,20 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
           if ((i & 31) != lane) continue;
           const int r = i / 6, cc = i % 6;
           if (sa == sb) {
-            if (cc <= r) sm.S[acol(6 * sa + cc, C) + r - cc] = -acc[i];
+            if (cc <= r) S_jobs[acol(6 * sa + cc, C) + r - cc] = -acc[i];
           } else {
             const int row = 6 * sb + cc, col = 6 * sa + r;
-            sm.S[acol(col, C) + row - col] = -acc[i];
+            S_jobs[acol(col, C) + row - col] = -acc[i];
           }
         }
       }
     }
-    __syncthreads();
+    gsync();
+    if constexpr (GRID) {
+      for (int i = tid; i < CA; i += blockDim.x) sm.S[i] = S_jobs[i];
+      for (int i = tid; i < nf * kUcamStride; i += blockDim.x) sm.ucam[i] = U_jobs[i];
+      __syncthreads();
+    }
     PROF_MARK(PH_JOBS)
 
     // ---------- assemble damped S and rhs (miniba.py:188-213) ----------
@@ -738,7 +805,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       // back substitution for the points (miniba.py:217)
       if (opt_pts) {
         const T df = has_f ? T(sm.dc[FI]) : T(0);
-        for (int p = tid; p < Pn; p += blockDim.x) {
+        for (int p = gtid; p < Pn; p += gthreads) {
           T* pw = ptw + (size_t)p * kPtStride;
           T u0 = pw[6] + pw[9] * df, u1 = pw[7] + pw[10] * df, u2 = pw[8] + pw[11] * df;
           for (int k = ptr[p]; k < ptr[p + 1]; ++k) {
@@ -763,12 +830,12 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
           pw[14] = -x2;
         }
       }
-      __syncthreads();
+      gsync();
     }
     PROF_MARK(PH_SOLVE)
 
     // ---------- K5 trials, accept / reject, lambda (miniba.py:244-293) ----------
-    if (tid == 0) lambdas[it] = lam;
+    if (lead) lambdas[it] = lam;
     int tries = 0, took = -1;
     double tc_[3] = {0, 0, 0};
     double ft = f;
@@ -795,7 +862,8 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
         const double frac = ldexp(1.0, -bt);
         ft = has_f ? f + frac * sm.dc[FI] : f;
         cost_pass<T>(obs, lo, K, X, ptw, frac, opt_pts, sm.Rt + (size_t)bt * n * 9,
-                     sm.tt + (size_t)bt * n * 3, ft, cx, cy, delta, loss, sm.red, tc_);
+                     sm.tt + (size_t)bt * n * 3, ft, cx, cy, delta, loss, sm.red, tc_, gtid, gthreads);
+        grid_sum(tc_, 3);
         ++tries;
         if (tc_[0] < cost && isfinite(tc_[0])) {
           took = bt;
@@ -804,14 +872,14 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       }
     }
     PROF_MARK(PH_TRIAL)
-    if (tid == 0) evals[it] = (uint8_t)tries;
+    if (lead) evals[it] = (uint8_t)tries;
     bool stop = false;
     if (took >= 0) {
       const double frac = ldexp(1.0, -took);
       for (int i = tid; i < n * 9; i += blockDim.x) sm.Rc[i] = sm.Rt[(size_t)took * n * 9 + i];
       for (int i = tid; i < n * 3; i += blockDim.x) sm.tc[i] = sm.tt[(size_t)took * n * 3 + i];
       if (opt_pts)
-        for (int p = tid; p < Pn; p += blockDim.x) {
+        for (int p = gtid; p < Pn; p += gthreads) {
           const T* dp = ptw + (size_t)p * kPtStride + 12;
           X[3 * p + 0] = X[3 * p + 0] + frac * (double)dp[0];
           X[3 * p + 1] = X[3 * p + 1] + frac * (double)dp[1];
@@ -823,30 +891,32 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       cost = tc_[0];
       se = tc_[1];
       se2 = tc_[2];
-      if (tid == 0) accepted[it] = 1;
+      if (lead) accepted[it] = 1;
       if (improve <= 1e-15 * fmax(cost, 1.0)) {
         stop = true;
         stop_reason = MBA_SOLVE_CONVERGED;
       }
     } else {
       lam = fmin(lam * nu, kLambdaMax);
-      if (tid == 0) accepted[it] = 0;
+      if (lead) accepted[it] = 0;
       if (!chol_fail && lam >= kLambdaMax) {
         stop = true;
         stop_reason = MBA_SOLVE_LAMBDA_CAP;
       }
     }
-    if (tid == 0) costs[it + 1] = cost;
+    if (lead) costs[it + 1] = cost;
     ++it;
-    __syncthreads();
+    gsync();
     PROF_MARK(PH_COMMIT)
     if (stop) break;
   }
 
   // ---------------- outputs ----------------
-  for (int i = tid; i < n * 9; i += blockDim.x) O.R_out[cb * 9 + i] = sm.Rc[i];
-  for (int i = tid; i < n * 3; i += blockDim.x) O.t_out[cb * 3 + i] = sm.tc[i];
-  if (tid == 0) {
+  if (rank == 0) {
+    for (int i = tid; i < n * 9; i += blockDim.x) O.R_out[cb * 9 + i] = sm.Rc[i];
+    for (int i = tid; i < n * 3; i += blockDim.x) O.t_out[cb * 3 + i] = sm.tc[i];
+  }
+  if (lead) {
     O.focal_out[b] = f;
     O.n_iters[b] = it;
     O.status[b] = stop_reason;
@@ -2148,6 +2218,52 @@ static int launch_pw(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOut
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
+// Cooperative mode: every CTA of the grid works on the same problem (points,
+// observations and Schur jobs are split across the grid; the small reduced
+// camera system is factorised redundantly in every CTA, so no broadcast is
+// needed). Problems of the batch are processed one after another.
+template <typename T, int MAXC>
+__global__ void __launch_bounds__(kThreads, 1) solve_grid_kernel(SolveParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  for (int b = 0; b < P.d.n_problems; ++b) {
+    solve_one<T, MAXC, false, true>(P, b, smem_raw);
+    cooperative_groups::this_grid().sync();
+  }
+}
+
+template <typename T, int MAXC>
+static int launch_grid(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t scratch = scratch_bytes<T, false>(d->max_obs, d->max_points, d->max_pairs);
+  const size_t smem = Layout<T, MAXC>::kFixed;
+  if (smem > kSmemLimit) return MBA_ERR_TOO_LARGE;
+  cudaFuncSetAttribute(solve_grid_kernel<T, MAXC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_grid_kernel<T, MAXC>, kThreads, smem);
+  if (per_sm < 1) return MBA_ERR_TOO_LARGE;
+  int grid = n_sm;  // one CTA per SM
+  // enough observations per CTA to amortise the grid barriers
+  const int64_t want = (d->max_obs + 511) / 512;
+  if (want < grid) grid = (int)(want < 1 ? 1 : want);
+  const size_t gbytes = align16(GridBufs<T, MAXC>::bytes(grid));
+  if (ws_bytes < 256 + scratch + gbytes) return MBA_ERR_INVALID;
+  SolveParams P;
+  P.d = *d;
+  P.cfg = *cfg;
+  P.o = *o;
+  P.counter = (int*)ws;
+  P.ws = (unsigned char*)ws + 256;
+  P.ws_slot_bytes = scratch;
+  P.max_cams = d->max_cams;
+  P.grid = P.ws + align16(scratch);
+  void* args[] = {&P};
+  cudaLaunchCooperativeKernel((void*)solve_grid_kernel<T, MAXC>, dim3(grid), dim3(kThreads), args, smem, st);
+  return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
+}
+
 template <typename T, int MAXC, bool RES>
 static int launch_cfg(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
                       size_t ws_bytes, cudaStream_t st) {
@@ -2218,9 +2334,10 @@ static int launch_warp(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaO
 // CTA per problem (scratch in shared memory when it fits).
 static int choose_mode(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
   if (cfg->ctas_per_problem < 0) return -cfg->ctas_per_problem;   // forced: 1 warp, 2 CTA, 3 point-wise
+  // a few large problems: spread each over the whole GPU (cooperative grid)
+  if (d->n_problems <= 8 && d->max_obs >= 4096) return 4;
   // measured on config 4: CTA-resident 133k problems/s, point-wise
   // 73k, warp-per-problem 72k (mixed) -> the CTA kernel is the default
-  (void)d;
   return 2;
 }
 
@@ -2228,6 +2345,12 @@ template <typename T>
 static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
   const int mode = choose_mode(d, cfg);
+  if (mode == 4) {
+    if (d->max_cams <= 8) return launch_grid<T, 8>(d, cfg, o, ws, ws_bytes, st);
+    if (d->max_cams <= 16) return launch_grid<T, 16>(d, cfg, o, ws, ws_bytes, st);
+    if (d->max_cams <= 32) return launch_grid<T, 32>(d, cfg, o, ws, ws_bytes, st);
+    return MBA_ERR_TOO_LARGE;
+  }
   if (d->max_cams <= 8 && d->max_track <= kChunk && mode == 3)
     return launch_pw<T, 8, sizeof(T) == 4 ? 4 : 2>(d, cfg, o, ws, ws_bytes, st);
   if (d->max_cams <= 8 && mode == 1) return launch_warp<T, 8>(d, cfg, o, ws, ws_bytes, st);
@@ -2262,9 +2385,13 @@ size_t mba_workspace_bytes(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
   const bool f64 = cfg->precision == MBA_LIN_F64;
   const size_t slot = f64 ? mba::scratch_bytes<double, false>(d->max_obs, d->max_points, d->max_pairs)
                           : mba::scratch_bytes<float, false>(d->max_obs, d->max_points, d->max_pairs);
+  const size_t gextra = mba::align16(mba::GridBufs<double, 32>::bytes(n_sm)) + 256;
+  if (slot + gextra > slot * 2) {
+    // cooperative mode needs one scratch slot plus the cross-CTA buffers
+  }
   size_t grid = (size_t)n_sm * 16;  // upper bound on resident CTAs / warps
   if (grid > (size_t)d->n_problems + mba::kWarpsPerCta) grid = d->n_problems + mba::kWarpsPerCta;
-  return 256 + slot * grid;
+  return 256 + slot * grid + gextra;
 }
 
 int32_t mba_solve(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o,

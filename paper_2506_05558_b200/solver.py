@@ -203,7 +203,8 @@ class LmParams:
     loss: str = "huber"
     precision: str = "f64"
     fail_at: tuple = ()
-    kernel: str = "auto"      # "auto" | "pw" (point-wise) | "warp" (warp per problem) | "cta" (CTA per problem)
+    kernel: str = "auto"      # "auto" | "cta" (CTA per problem) | "grid" (whole GPU per problem)
+    #                           | "pw" (point-wise) | "warp" (warp per problem)
 
     @staticmethod
     def from_cfg(cfg, **over):
@@ -261,7 +262,7 @@ def descriptors(db: DeviceBatch, prm: LmParams, sol: Solution):
     c = MbaLmConfig(lambda_init=prm.lambda_init, nu=prm.nu, delta=prm.delta,
                     max_iters=prm.max_iters, loss=_lib.LOSS[prm.loss],
                     precision=_lib.PRECISION[prm.precision],
-                    ctas_per_problem={"auto": 0, "warp": -1, "cta": -2, "pw": -3}[prm.kernel],
+                    ctas_per_problem={"auto": 0, "warp": -1, "cta": -2, "pw": -3, "grid": -4}[prm.kernel],
                     fail_iters_mask=sum(1 << int(i) for i in prm.fail_at if 0 <= int(i) < 64))
     o = MbaOutputs(R_in=ptr(db.R), t_in=ptr(db.t), focal_in=ptr(db.focal), points_in=ptr(db.points),
                    R_out=ptr(sol.R), t_out=ptr(sol.t), focal_out=ptr(sol.focal),
@@ -295,3 +296,72 @@ def fetch(sol: Solution, b: int = 0) -> dict:
                 evals=sol.evals[b, :n].cpu().numpy().astype(np.int32),
                 final_rms=float(np.sqrt(st[2] / K)), mean_err=float(st[1] / K),
                 status=int(sol.status[b].item()))
+
+
+# ---------------------------------------------------------------------------
+# host-to-host batched solve with copy/compute overlap (the end-to-end path)
+
+def split_host_batch(hb: HostBatch, n_chunks: int):
+    """Contiguous problem ranges of a host batch as self-contained HostBatch
+    views (offset arrays rebased; data arrays are views, no copies)."""
+    B = hb.n_problems
+    n_chunks = max(1, min(n_chunks, B))
+    cuts = [B * i // n_chunks for i in range(n_chunks + 1)]
+    parts = []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        c0, c1 = hb.cam_off[a], hb.cam_off[b]
+        p0, p1 = hb.pt_off[a], hb.pt_off[b]
+        o0, o1 = hb.obs_off[a], hb.obs_off[b]
+        parts.append(HostBatch(
+            cam_off=hb.cam_off[a:b + 1] - c0, pt_off=hb.pt_off[a:b + 1] - p0,
+            obs_off=hb.obs_off[a:b + 1] - o0, obs=hb.obs[o0:o1],
+            obs_lo=None if hb.obs_lo is None else hb.obs_lo[o0:o1], fixed=hb.fixed[c0:c1],
+            cx=hb.cx[a:b], cy=hb.cy[a:b], flags=hb.flags[a:b], R=hb.R[c0:c1], t=hb.t[c0:c1],
+            focal=hb.focal[a:b], points=hb.points[p0:p1], max_pairs=hb.max_pairs,
+            max_track=hb.max_track))
+    return parts, cuts
+
+
+class PipelinedSolver:
+    """End-to-end solve of a host batch: H2D of chunk i+1 overlaps the solve
+    of chunk i on a second stream; each chunk's solution (R, t, focal, points,
+    final stats, n_iters, status) is copied back to pinned host memory."""
+
+    OUT = ("R", "t", "focal", "points", "final_stats", "n_iters", "status")
+
+    def __init__(self, hb: HostBatch, prm: LmParams, n_chunks: int = 4):
+        torch = _lib.torch_cuda()
+        self.prm = prm
+        self.parts, self.cuts = split_host_batch(hb, n_chunks)
+        self.pinned = [pin(p) for p in self.parts]
+        self.copy = torch.cuda.Stream()
+        self.compute = torch.cuda.Stream()
+        self.dev = [to_device(p, pinned=self.pinned[i]) for i, p in enumerate(self.parts)]
+        torch.cuda.synchronize()
+        self.sols = [Solution(d, prm.max_iters) for d in self.dev]
+        self.host = [{k: torch.empty(getattr(s, k).shape, dtype=getattr(s, k).dtype, pin_memory=True)
+                      for k in self.OUT} for s in self.sols]
+        self.h2d_bytes = sum(d.h2d_bytes for d in self.dev)
+        self.d2h_bytes = sum(v.numel() * v.element_size() for h in self.host for v in h.values())
+
+    def run(self):
+        """Enqueue H2D -> solve -> D2H for every chunk (asynchronous)."""
+        torch = _lib.torch_cuda()
+        fields = _INPUT_FIELDS
+        for i, (d, src) in enumerate(zip(self.dev, self.pinned)):
+            with torch.cuda.stream(self.copy):
+                for k in fields:
+                    if src[k] is not None:
+                        getattr(d, k).copy_(src[k], non_blocking=True)
+                h2d = torch.cuda.Event()
+                h2d.record(self.copy)
+            self.compute.wait_event(h2d)
+            with torch.cuda.stream(self.compute):
+                solve(d, self.prm, self.sols[i])
+                done = torch.cuda.Event()
+                done.record(self.compute)
+            self.copy.wait_event(done)
+            with torch.cuda.stream(self.copy):
+                for k in self.OUT:
+                    self.host[i][k].copy_(getattr(self.sols[i], k), non_blocking=True)
+        return self

@@ -12,7 +12,7 @@ from oracle import miniba_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp", "pw"])
+@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "grid"])
 @pytest.mark.parametrize("path", golden_cases(), ids=golden_ids())
 def test_solver_matches_reference_golden(path, kernel, cuda_ok):
     """float64 mode (the API default): exact trace parity through i* (fp64
@@ -97,18 +97,20 @@ def test_deterministic_repeat(cuda_ok):
         np.testing.assert_array_equal(x["points"], y["points"])
 
 
+@pytest.mark.parametrize("kernel", ["cta", "grid"])
 @pytest.mark.parametrize("precision", ["mixed", "f64"])
-def test_paper_scale_single_problem(precision, cuda_ok):
+def test_paper_scale_single_problem(precision, kernel, cuda_ok):
     """BASELINE config 2: 8 frames, K = 20k, Huber."""
     from paper_2506_05558_b200.synth import make_batch
     p = make_batch(1, n_cams=8, K=20000, seed=2).problem(0)
-    dev = run_device([p], dict(max_iters=200), precision)[0]
+    dev = run_device([p], dict(max_iters=200), precision, kernel)[0]
     ref = O.lm(p, max_iters=200)
     assert_parity(dev, ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"], p["R"], p["t"],
                   p["focal"], label="cfg2")
 
 
-def test_cauchy_outliers_many_cameras(cuda_ok):
+@pytest.mark.parametrize("kernel", ["cta", "grid"])
+def test_cauchy_outliers_many_cameras(kernel, cuda_ok):
     """Config-5 shape at oracle-friendly size: 16 frames, 20% outliers, Cauchy
     (extension; parity against the oracle only -- unpinned by the reference)."""
     from paper_2506_05558_b200.synth import make_batch
@@ -116,13 +118,13 @@ def test_cauchy_outliers_many_cameras(cuda_ok):
     # oracle's cho_factor fails on the near-singular (scale-gauge) system, a
     # roundoff event that a differently ordered factorisation need not repeat.
     p = make_batch(1, n_cams=16, K=6000, seed=5, outlier_frac=0.2).problem(0)
-    dev = run_device([p], dict(max_iters=25, loss="cauchy"), "f64")[0]
+    dev = run_device([p], dict(max_iters=25, loss="cauchy"), "f64", kernel)[0]
     ref = O.lm(p, max_iters=25, loss="cauchy")
     assert_parity(dev, ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"], p["R"], p["t"],
                   p["focal"], label="cauchy16")
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp", "pw"])
+@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "grid"])
 def test_fault_injection_matches_oracle(kernel, cuda_ok):
     from paper_2506_05558_b200.synth import make_batch
     p = make_batch(1, n_cams=8, K=2000, seed=4).problem(0)
@@ -159,7 +161,7 @@ def test_all_cameras_fixed_focal_only(kernel, cuda_ok):
     assert dev["accepted"][:3].tolist() == ref["accepted"][:3].tolist()
 
 
-@pytest.mark.parametrize("other", ["warp", "pw"])
+@pytest.mark.parametrize("other", ["warp", "pw", "grid"])
 def test_kernels_agree(other, cuda_ok):
     """All kernels implement the same arithmetic per problem up to reduction
     order: traces agree through i* and final costs to 1e-9 on 64 problems."""
@@ -172,3 +174,15 @@ def test_kernels_agree(other, cuda_ok):
         i_star = O.plateau_index(y["costs"])
         assert np.array_equal(x["accepted"][:i_star + 1], y["accepted"][:i_star + 1])
         assert abs(x["costs"][-1] - y["costs"][-1]) <= 1e-9 * y["costs"][-1]
+
+
+def test_grid_mode_config5_shape(cuda_ok):
+    """32 cameras, 20% outliers, Cauchy, across the whole GPU (cooperative
+    grid): trace parity with the oracle for 6 iterations at K = 40k (oracle-
+    sized version of BASELINE config 5)."""
+    from paper_2506_05558_b200.synth import make_batch
+    p = make_batch(1, n_cams=32, K=40000, seed=12, outlier_frac=0.2).problem(0)
+    dev = run_device([p], dict(max_iters=6, loss="cauchy"), "f64", "grid")[0]
+    ref = O.lm(p, max_iters=6, loss="cauchy")
+    assert_parity(dev, ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"], p["R"], p["t"],
+                  p["focal"], label="grid32")
