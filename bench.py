@@ -143,12 +143,12 @@ class ClockSampler:
 
 def _cpu_solve(args):
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    c, idx, seed = args
+    c, idx, seed, max_iters = args
     from oracle import miniba_oracle as O
     b = make_shard(c, idx, 1, seed=seed)
     p = b.problem(0)
     t0 = time.perf_counter()
-    info = O.lm(p, max_iters=c["max_iters"], loss=c["loss"])
+    info = O.lm(p, max_iters=max_iters, loss=c["loss"])
     return time.perf_counter() - t0, len(info["accepted"])
 
 
@@ -157,6 +157,14 @@ def cpu_reference(c, budget_s=15.0, seed=0):
     time budget is used. Returns (problems/s, iterations/s, cores, sample)."""
     import multiprocessing as mp
     cores = len(os.sched_getaffinity(0))
+    if c["n_problems"] == 1 and c["K"] >= 100000:
+        # one stress problem: a full 50-iteration CPU solve takes ~20 min, so
+        # time the first 2 LM iterations on one core and scale to the solve
+        _pool_init()
+        sec, it = _cpu_solve((c, 0, seed, 2))
+        ips = it / sec
+        return (ips / c["max_iters"], ips, 1, f"first 2 LM iterations of the single problem, 1 core "
+                f"({sec:.1f} s); problems/s = iterations/s / {c['max_iters']}", sec)
     ctx = mp.get_context("spawn")
     done = iters = 0
     t0 = time.perf_counter()
@@ -165,7 +173,7 @@ def cpu_reference(c, budget_s=15.0, seed=0):
         pending = []
         while True:
             while len(pending) < 2 * cores and nxt < c["n_problems"] and time.perf_counter() - t0 < budget_s:
-                pending.append(pool.apply_async(_cpu_solve, ((c, nxt, seed),)))
+                pending.append(pool.apply_async(_cpu_solve, ((c, nxt, seed, c["max_iters"]),)))
                 nxt += 1
             if not pending:
                 break
@@ -173,8 +181,9 @@ def cpu_reference(c, budget_s=15.0, seed=0):
             done += 1
             iters += r[1]
     el = time.perf_counter() - t0
+    used = min(cores, max(done, 1))
     sample = f"first {done} problems of the workload, full LM solves, {cores} worker processes"
-    return done / el, iters / el, cores, sample, el
+    return done / el, iters / el, used, sample, el
 
 
 def _pool_init():
@@ -224,13 +233,14 @@ def main():
 
     import torch
     import torch.distributed as dist
+    from paper_2506_05558_b200 import dist as mdist
     from paper_2506_05558_b200 import solver
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = c["n_problems"]
-    lo, hi = B * rank // world, B * (rank + 1) // world
+    lo, hi = mdist.shard_range(B, rank, world)
     t_gen = time.perf_counter()
     batch = make_shard(c, lo, hi - lo, workers=max(1, len(os.sched_getaffinity(0)) // max(world, 1)))
     hb = solver.pack_synth(batch)
@@ -244,21 +254,16 @@ def main():
     flush = None if in_bytes > l2_bytes else torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda")
     cfg_json["l2"] = ("inputs larger than L2 (%.2f GB per rank)" % (in_bytes / 1e9) if flush is None
                       else "L2 flushed (256 MB write) between timed steps")
-    summary = torch.empty((hi - lo, 6), dtype=torch.float64, device="cuda")
-    gather = None
-    if world > 1:
-        gather = torch.empty(((B + world - 1) // world * world, 6), dtype=torch.float64, device="cuda")
+    rows = mdist.padded_rows(B, world)
+    gbufs = [torch.empty((rows, mdist.SUMMARY_WIDTH), dtype=torch.float64, device="cuda")
+             for _ in range(world)]
 
     def gather_step():
+        """final gather of the per-problem summaries (the only collective)"""
         if world == 1:
-            return
-        summary[:, :4] = sol.final_stats
-        summary[:, 4] = sol.n_iters.double()
-        summary[:, 5] = sol.status.double()
-        per = (B + world - 1) // world
-        pad = torch.zeros((per, 6), dtype=torch.float64, device="cuda")
-        pad[:hi - lo] = summary
-        dist.all_gather_into_tensor(gather, pad)
+            return None
+        local = mdist.pack_summary(torch, sol.final_stats, sol.n_iters, sol.status, rows, "cuda")
+        return mdist.gather_summaries(torch, dist, local, B, world, gbufs)
 
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):

@@ -2289,8 +2289,34 @@ static int launch_cfg(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOu
   P.ws_slot_bytes = scratch;
   P.max_cams = d->max_cams;
   cudaMemsetAsync(ws, 0, sizeof(int), st);
+  // Keep the per-CTA scratch slots resident in L2 (persisting window) while
+  // the observation stream passes through; the caller's stream attribute is
+  // restored after the launch.
+  cudaStreamAttrValue old_attr{}, attr{};
+  bool windowed = false;
+  if (!RES) {
+    int max_win = 0, max_persist = 0;
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    const size_t want = scratch * (size_t)grid;
+    if (max_win > 0 && max_persist > 0 &&
+        cudaStreamGetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &old_attr) == cudaSuccess) {
+      size_t limit = 0;
+      cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize);
+      if (limit < (size_t)max_persist) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+      attr.accessPolicyWindow.base_ptr = P.ws;
+      attr.accessPolicyWindow.num_bytes = want < (size_t)max_win ? want : (size_t)max_win;
+      attr.accessPolicyWindow.hitRatio = 1.0f;
+      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      windowed = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr) == cudaSuccess;
+    }
+    cudaGetLastError();
+  }
   solve_kernel<T, MAXC, RES><<<grid, kThreads, smem, st>>>(P);
-  return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
+  const cudaError_t err = cudaGetLastError();
+  if (windowed) cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &old_attr);
+  return err == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
 }
 
 // Shared-memory-resident scratch when the largest problem of the batch fits,

@@ -247,6 +247,26 @@ def main():
                         Rf_out=Rf, tf_out=tf, costf_out=cf)
     print("pose_lm written")
 
+    # ---- bootstrap (the production caller of lm_solve, miniba.py:729-854) ----
+    for seed in (0, 1):
+        bp = S.bootstrap_problem(seed, n_cams=8, n_points=300, noise_px=0.5)
+        poses, intr_out, table, info = M.bootstrap(bp["features"], bp["intr"], cfg,
+                                                   matcher=bp["matcher"])
+        kp = np.concatenate([f[0] for f in bp["features"]])
+        ids = np.concatenate([f[1] for f in bp["features"]])
+        counts = np.array([len(f[1]) for f in bp["features"]])
+        np.savez_compressed(os.path.join(HERE, f"bootstrap_seed{seed}.npz"),
+                            keypoints=kp, ids=ids, counts=counts, focal=bp["intr"].focal,
+                            cx=bp["intr"].cx, cy=bp["intr"].cy, width=bp["intr"].width,
+                            height=bp["intr"].height,
+                            out_R=np.stack([p.R for p in poses]),
+                            out_t=np.stack([p.translation for p in poses]),
+                            out_focal=intr_out.focal, out_n_tracks=info["n_tracks"],
+                            out_mean_err=info["mean_err"], out_rescued=info["rescued"],
+                            out_costs=info["costs"])
+        print(f"bootstrap seed {seed}: focal {intr_out.focal:.3f} tracks {info['n_tracks']} "
+              f"rescued {info['rescued']}")
+
 
 if __name__ == "__main__":
     main()

@@ -81,3 +81,41 @@ def test_dense_lm_solve_path(cuda_ok):
     info = M.lm_solve(prob, LmConfig(max_iters=int(z["max_iters"])), method="dense")
     np.testing.assert_allclose(info["costs"][-1], z["out_costs"][-1], rtol=1e-8)
     assert info["accepted"][:5].tolist() == z["out_accepted"][:5].tolist()
+
+
+def _exact_matcher(feat_a, feat_b):
+    """Fake matcher of the reference's oracle (synthetic.py:313-327): the
+    'descriptors' are ground-truth point ids."""
+    pos_b = {int(v): j for j, v in enumerate(feat_b[1])}
+    ia, ib = [], []
+    for i, v in enumerate(feat_a[1]):
+        j = pos_b.get(int(v))
+        if j is not None:
+            ia.append(i)
+            ib.append(j)
+    return np.array(ia, dtype=np.int64), np.array(ib, dtype=np.int64), np.zeros(len(ia))
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_bootstrap_matches_reference(seed, cuda_ok):
+    """Bootstrap (miniba.py:729-854: tracks, 100 + 100 LM iterations with the
+    median + 4 MAD filter between, gauge normalisation) on the reference's own
+    bootstrap oracle problem, against the reference's output."""
+    from gsrecon import miniba as M
+    from gsrecon.config import CaptureConfig
+    from gsrecon.scene import CameraIntrinsics
+    z = np.load(f"{GOLDEN}/bootstrap_seed{seed}.npz")
+    feats, o = [], 0
+    for c in z["counts"]:
+        feats.append((z["keypoints"][o:o + c], z["ids"][o:o + c]))
+        o += c
+    intr = CameraIntrinsics(float(z["focal"]), float(z["cx"]), float(z["cy"]), int(z["width"]),
+                            int(z["height"]))
+    poses, intr_out, table, info = M.bootstrap(feats, intr, CaptureConfig(), matcher=_exact_matcher)
+    assert info["n_tracks"] == int(z["out_n_tracks"])
+    assert bool(info["rescued"]) == bool(z["out_rescued"])
+    np.testing.assert_allclose(intr_out.focal, float(z["out_focal"]), rtol=1e-6)
+    for p, R, t in zip(poses, z["out_R"], z["out_t"]):
+        np.testing.assert_allclose(p.R, R, atol=1e-6)
+        np.testing.assert_allclose(p.translation, t, atol=1e-6)
+    np.testing.assert_allclose(info["mean_err"], float(z["out_mean_err"]), rtol=1e-6)
