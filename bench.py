@@ -206,6 +206,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=4)
+    ap.add_argument("--kernel", default="auto", help="solver kernel (LmParams.kernel)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -214,7 +215,7 @@ def main():
     c = workload(args.config, args.problems)
     cfg_json = {"workload": f"config{args.config}: {c['desc']}", "n_problems": c["n_problems"],
                 "n_cams": c["n_cams"], "K": c["K"], "loss": c["loss"], "max_iters": c["max_iters"],
-                "precision": args.precision}
+                "precision": args.precision, "kernel": args.kernel}
 
     if args.impl == "reference":
         if rank != 0:
@@ -245,7 +246,8 @@ def main():
     batch = make_shard(c, lo, hi - lo, workers=max(1, len(os.sched_getaffinity(0)) // max(world, 1)))
     hb = solver.pack_synth(batch)
     t_gen = time.perf_counter() - t_gen
-    prm = solver.LmParams(max_iters=c["max_iters"], loss=c["loss"], precision=args.precision)
+    prm = solver.LmParams(max_iters=c["max_iters"], loss=c["loss"], precision=args.precision,
+                          kernel=args.kernel)
     pinned = solver.pin(hb)
     db = solver.to_device(hb, pinned=pinned)
     sol = solver.Solution(db, prm.max_iters)

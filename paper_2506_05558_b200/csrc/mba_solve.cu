@@ -37,12 +37,14 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
 #include <cooperative_groups.h>
 
 #include "mba_common.cuh"
+#include "mba_v4.cuh"
 
 namespace mba {
 
@@ -77,6 +79,7 @@ struct SolveParams {
   size_t ws_slot_bytes;
   int max_cams;
   unsigned char* grid;     // cooperative (multi-CTA) mode: cross-CTA buffers
+  int only_flagged;        // solve only problems the cluster kernel could not place
 };
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -309,8 +312,9 @@ struct GridBufs {
   static __host__ __device__ size_t bytes(int G) { return oRed + 8 * 2 * 4 * (size_t)G; }
 };
 
-template <typename T, int MAXC, bool RES, bool GRID = false>
+template <typename T, int MAXC, bool RES, bool GRID = false, int NT = kThreads>
 __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) {
+  constexpr int kWarps = NT / 32;
   using L = Layout<T, MAXC>;
   using GB = GridBufs<T, MAXC>;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -929,8 +933,8 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   __syncthreads();
 }
 
-template <typename T, int MAXC, bool RES>
-__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && !RES) ? 2 : 1) solve_kernel(SolveParams P) {
+template <typename T, int MAXC, bool RES, int NT = kThreads, int MINB = (sizeof(T) == 4 && !RES) ? 2 : 1>
+__global__ void __launch_bounds__(NT, MINB) solve_kernel(SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_prob;
   for (;;) {
@@ -939,7 +943,8 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && !RES) ? 2 : 1) so
     const int b = s_prob;
     __syncthreads();
     if (b >= P.d.n_problems) return;
-    solve_one<T, MAXC, RES>(P, b, smem_raw);
+    if (P.only_flagged && P.o.status[b] != v4::kStatusPlanOverflow) continue;
+    solve_one<T, MAXC, RES, false, NT>(P, b, smem_raw);
   }
 }
 
@@ -2264,18 +2269,19 @@ static int launch_grid(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaO
   return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
 }
 
-template <typename T, int MAXC, bool RES>
+template <typename T, int MAXC, bool RES, int NT = kThreads, int MINB = (sizeof(T) == 4 && !RES) ? 2 : 1>
 static int launch_cfg(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
-                      size_t ws_bytes, cudaStream_t st) {
+                      size_t ws_bytes, cudaStream_t st, int only_flagged = 0) {
   int dev = 0, n_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   const size_t scratch = scratch_bytes<T, RES>(d->max_obs, d->max_points, d->max_pairs);
   const size_t smem = Layout<T, MAXC>::kFixed + (RES ? scratch : 0);
   if (smem > kSmemLimit) return MBA_ERR_TOO_LARGE;
-  cudaFuncSetAttribute(solve_kernel<T, MAXC, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(solve_kernel<T, MAXC, RES, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<T, MAXC, RES>, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<T, MAXC, RES, NT, MINB>, NT, smem);
+  if (const char* e = getenv("MBA_PER_SM")) { int v = atoi(e); if (v > 0 && v < per_sm) per_sm = v; }
   if (per_sm < 1) return MBA_ERR_TOO_LARGE;
   int grid = n_sm * per_sm;
   if (grid > d->n_problems) grid = d->n_problems;
@@ -2288,6 +2294,7 @@ static int launch_cfg(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOu
   P.ws = (unsigned char*)ws + 256;
   P.ws_slot_bytes = scratch;
   P.max_cams = d->max_cams;
+  P.only_flagged = only_flagged;
   cudaMemsetAsync(ws, 0, sizeof(int), st);
   // Keep the per-CTA scratch slots resident in L2 (persisting window) while
   // the observation stream passes through; the caller's stream attribute is
@@ -2313,7 +2320,7 @@ static int launch_cfg(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOu
     }
     cudaGetLastError();
   }
-  solve_kernel<T, MAXC, RES><<<grid, kThreads, smem, st>>>(P);
+  solve_kernel<T, MAXC, RES, NT, MINB><<<grid, NT, smem, st>>>(P);
   const cudaError_t err = cudaGetLastError();
   if (windowed) cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &old_attr);
   return err == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
@@ -2364,6 +2371,7 @@ static int choose_mode(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
   if (d->n_problems <= 8 && d->max_obs >= 4096) return 4;
   // measured on config 4: CTA-resident 133k problems/s, point-wise
   // 73k, warp-per-problem 72k (mixed) -> the CTA kernel is the default
+  if (getenv("MBA_AUTO_V4")) return 0;
   return 2;
 }
 
@@ -2371,6 +2379,17 @@ template <typename T>
 static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
   const int mode = choose_mode(d, cfg);
+  if (mode == 9 || mode == 0) {
+    // cluster-resident kernel; problems whose slices overflow its shared-memory
+    // plan are re-solved by the CTA kernel (restricted to flagged problems)
+    const int R = v4::plan_cluster(d, cfg);
+    if (R > 0) {
+      int rc = v4::launch(d, cfg, o, st, R);
+      if (rc != MBA_OK) return rc;
+      return launch_cfg<T, 8, false>(d, cfg, o, ws, ws_bytes, st, 1);
+    }
+    if (mode == 9) return MBA_ERR_TOO_LARGE;
+  }
   if (mode == 4) {
     if (d->max_cams <= 8) return launch_grid<T, 8>(d, cfg, o, ws, ws_bytes, st);
     if (d->max_cams <= 16) return launch_grid<T, 16>(d, cfg, o, ws, ws_bytes, st);
@@ -2380,6 +2399,10 @@ static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutput
   if (d->max_cams <= 8 && d->max_track <= kChunk && mode == 3)
     return launch_pw<T, 8, sizeof(T) == 4 ? 4 : 2>(d, cfg, o, ws, ws_bytes, st);
   if (d->max_cams <= 8 && mode == 1) return launch_warp<T, 8>(d, cfg, o, ws, ws_bytes, st);
+  if (d->max_cams <= 8 && mode == 5) return launch_cfg<T, 8, false, 256, 2>(d, cfg, o, ws, ws_bytes, st);
+  if (d->max_cams <= 8 && mode == 6) return launch_cfg<T, 8, false, 128, 4>(d, cfg, o, ws, ws_bytes, st);
+  if (d->max_cams <= 8 && mode == 7) return launch_cfg<T, 8, false, 128, 3>(d, cfg, o, ws, ws_bytes, st);
+  if (d->max_cams <= 8 && mode == 8) return launch_cfg<T, 8, false, 64, 6>(d, cfg, o, ws, ws_bytes, st);
   if (d->max_cams <= 8) {
     if (resident_fits<T, 8>(d)) return launch_cfg<T, 8, true>(d, cfg, o, ws, ws_bytes, st);
     return launch_cfg<T, 8, false>(d, cfg, o, ws, ws_bytes, st);

@@ -1,0 +1,1124 @@
+// mba_v4.cu -- cluster-resident Levenberg-Marquardt mini-BA (sm_100a).
+//
+// Same algorithm as solve_kernel (mba_solve.cu) -- lm_solve, miniba.py:223-296,
+// with residuals (85-98), huber/cauchy weights (46-54), _build_blocks
+// (101-132), _assemble (135-177) and solve_step(method="schur") (180-220) --
+// re-mapped so that a problem's whole working set lives in SHARED MEMORY:
+//
+//  * One thread-block cluster of R CTAs per problem (R = 1, 2, 4, 8, 16 chosen
+//    by the host so the problem fits). CTA r owns a contiguous, point-aligned
+//    slice of the point-major observations; partial normal equations are
+//    summed across the cluster through distributed shared memory (DSMEM) in
+//    rank order, so every CTA holds a bit-identical reduced camera system and
+//    factorises it redundantly (no broadcast, no global memory traffic).
+//  * No per-observation Y = W V^-1/2 blocks are materialised. The point pass
+//    stores a COMPACT Jacobian per observation -- sqrt(w)*(f/z, -fx/z^2,
+//    -fy/z^2), v = R X, sqrt(w)*F, sqrt(w)*r (10 values) -- and the 3x3 point
+//    factor L_p. Schur products are rebuilt algebraically:
+//        A_i = Jp_i G_i,  G_i = [-[v_i]x | I],  B_i = Jp_i R_c,
+//        Q_i = B_i L_p^-T (2x3),
+//        Y_i Y_j^T = G_i^T (Jp_i^T (Q_i Q_j^T) Jp_j) G_j        (6x6)
+//    i.e. ~126 flops and 18 loads per co-observation pair instead of 108
+//    flops and 36 loads from an 18-value Y -- and 3x less memory, which is what
+//    lets the scratch stay on chip.
+//  * Camera jobs (U_aa, U_af, g_a, sum Y yf, sum Y z) and pair jobs
+//    (S_ab = -sum Y_i Y_j^T) are warps pulling from a shared-memory job queue;
+//    each job is reduced by a transposed warp butterfly (37-46 shuffles for 36-45
+//    sums instead of 180-225). Results do not depend on which warp ran a job.
+//  * LDL^T of the augmented reduced system (forward substitution fused), then a
+//    column-oriented back substitution in one warp (no reductions).
+//  * Trial cost passes read observations, points and the step from shared
+//    memory; the accept/reject / lambda logic is evaluated redundantly in every
+//    CTA of the cluster from identical sums.
+//
+// State (cameras, focal, points) is float64; T is the arithmetic type of the
+// linearise/Schur/LDL^T stages (double = "f64", float = "mixed").
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <cooperative_groups.h>
+
+#include "mba_common.cuh"
+#include "mba_v4.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mba {
+namespace v4 {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr int MAXN = 8;                          // cameras per problem
+constexpr int MAXC = 6 * MAXN + 1;               // reduced system size (+ focal)
+constexpr int MAXNB = MAXN * (MAXN + 1) / 2;     // camera blocks a <= b
+constexpr int CA_MAX = MAXC * (MAXC + 3) / 2;    // augmented packed size
+constexpr int JSTR = 11;   // per observation: J0 J1 J2 v0 v1 v2 F0 F1 r0 r1 (+pad, odd stride)
+constexpr int PSTR = 15;   // per point: iL00 L10 iL11 L20 L21 iL22 z0..2 yf0..2 dp0..2
+constexpr int UST = 45;    // camera job: U_aa(21) U_af(6) g_a(6) SYf(6) SYz(6)
+constexpr int JOB_PAIR0 = MAXN * UST;
+constexpr int JOB_PART = JOB_PAIR0 + MAXNB * 36;
+constexpr int JOB_OUT = JOB_PART + 4;
+constexpr size_t kSmemLimit = 227 * 1024;
+
+__host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ __forceinline__ int acol(int j, int C) { return j * (C + 1) - (j * (j - 1)) / 2; }
+
+template <typename T>
+struct Fixed {
+  static constexpr size_t oRc = 0;                                    // double[MAXN][9]
+  static constexpr size_t oTc = oRc + 8 * 9 * MAXN;                   // double[MAXN][3]
+  static constexpr size_t oRt = oTc + 8 * 3 * MAXN;                   // double[5][MAXN][9]
+  static constexpr size_t oTt = oRt + 8 * 9 * MAXN * kBacktrackTries; // double[5][MAXN][3]
+  static constexpr size_t oDc = oTt + 8 * 3 * MAXN * kBacktrackTries; // double[MAXC]
+  static constexpr size_t oXch = oDc + 8 * MAXC;                      // double[2][4] cluster exchange
+  static constexpr size_t oRed = oXch + 8 * 8;                        // double[NW][4]
+  static constexpr size_t oS = al16(oRed + 8 * NW * 4);               // T[CA_MAX]
+  static constexpr size_t oJob = al16(oS + sizeof(T) * CA_MAX);       // T[JOB_OUT] this CTA's partials
+  static constexpr size_t oJsum = al16(oJob + sizeof(T) * JOB_OUT);   // T[JOB_OUT] cluster sums
+  static constexpr size_t oInvd = al16(oJsum + sizeof(T) * JOB_OUT);  // T[MAXC]
+  static constexpr size_t oTab = al16(oInvd + sizeof(T) * MAXC);      // u16[CA_MAX] (row<<8|col)
+  static constexpr size_t oCamPtr = al16(oTab + 2 * CA_MAX);          // int[MAXN+1]
+  static constexpr size_t oSlot = oCamPtr + 4 * (MAXN + 1);           // int[MAXN]
+  static constexpr size_t oCos = oSlot + 4 * MAXN;                    // int[MAXN]
+  static constexpr size_t oBlkOff = oCos + 4 * MAXN;                  // int[MAXNB+1]
+  static constexpr size_t oBlkA = oBlkOff + 4 * (MAXNB + 1);          // u8[MAXNB]
+  static constexpr size_t oBlkB = oBlkA + MAXNB;                      // u8[MAXNB]
+  static constexpr size_t kBytes = al16(oBlkB + MAXNB);
+};
+
+// bytes per local observation / observed point in the arena (plus pairs, 4 B each)
+template <typename T>
+__host__ __device__ constexpr size_t obs_bytes() { return 16 + sizeof(T) * JSTR + 2; }
+template <typename T>
+__host__ __device__ constexpr size_t pt_bytes() { return 24 + sizeof(T) * PSTR + 4 + 2; }
+
+struct Params {
+  MbaBatchDesc d;
+  MbaLmConfig cfg;
+  MbaOutputs o;
+  size_t arena;   // bytes of dynamic shared memory after the fixed part
+};
+
+// ---------------------------------------------------------------------------
+// warp helpers
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+template <typename T, int N, int C, int H>
+__device__ __forceinline__ void rs_stage(T (&v)[N], int o, bool up) {
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const T lo = v[i];
+    T hi = T(0);
+    if (H + i < C) hi = v[(H + i) < N ? (H + i) : 0];
+    const T send = up ? lo : hi;
+    const T keep = up ? hi : lo;
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+  }
+}
+
+// Transposed warp reduction of N per-lane values: 5 halving butterfly stages
+// (sum(ceil(N/2^s)) shuffles instead of 5N); the total of value i is written to
+// out[i] by exactly one lane. Fixed order -> bit-reproducible.
+template <typename T, int N>
+__device__ __forceinline__ void warp_reduce_to(T (&v)[N], T* out, int lane) {
+  constexpr int h0 = (N + 1) / 2, h1 = (h0 + 1) / 2, h2 = (h1 + 1) / 2, h3 = (h2 + 1) / 2,
+                h4 = (h3 + 1) / 2;
+  rs_stage<T, N, N, h0>(v, 16, lane & 16);
+  rs_stage<T, N, h0, h1>(v, 8, lane & 8);
+  rs_stage<T, N, h1, h2>(v, 4, lane & 4);
+  rs_stage<T, N, h2, h3>(v, 2, lane & 2);
+  rs_stage<T, N, h3, h4>(v, 1, lane & 1);
+  const int b0 = lane & 1, b1 = (lane >> 1) & 1, b2 = (lane >> 2) & 1, b3 = (lane >> 3) & 1,
+            b4 = (lane >> 4) & 1;
+#pragma unroll
+  for (int j = 0; j < h4; ++j) {
+    int i = j + b0 * h4;
+    if (i >= h3) continue;
+    i += b1 * h3;
+    if (i >= h2) continue;
+    i += b2 * h2;
+    if (i >= h1) continue;
+    i += b3 * h1;
+    if (i >= h0) continue;
+    i += b4 * h0;
+    if (i >= N) continue;
+    out[i] = v[j];
+  }
+}
+
+// Deterministic block sum of N doubles (result to every thread).
+template <int N>
+__device__ __forceinline__ void block_sum_d(double (&v)[N], double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < N; ++i) red[wid * 4 + i] = v[i];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += red[w * 4 + i];
+    v[i] = s;
+  }
+  __syncthreads();
+}
+
+template <int R>
+struct Clu {
+  __device__ static __forceinline__ void sync() {
+    if constexpr (R > 1) cg::this_cluster().sync();
+    else __syncthreads();
+  }
+  __device__ static __forceinline__ int rank() {
+    if constexpr (R > 1) return (int)cg::this_cluster().block_rank();
+    else return 0;
+  }
+  template <typename U>
+  __device__ static __forceinline__ U* remote(U* p, int r) {
+    if constexpr (R > 1) return cg::this_cluster().map_shared_rank(p, r);
+    else return p;
+  }
+};
+
+// Cluster-wide sum of N (<= 4) doubles that every thread holds (after a block
+// sum); rank-ordered, so every CTA gets bit-identical totals. Double-buffered
+// exchange slots -> one cluster barrier per call.
+template <int R, int N>
+__device__ __forceinline__ void cluster_sum(double (&v)[N], double* xch, int& epoch) {
+  if constexpr (R > 1) {
+    double* slot = xch + 4 * (epoch & 1);
+    ++epoch;
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int i = 0; i < N; ++i) slot[i] = v[i];
+    Clu<R>::sync();
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double* q = Clu<R>::remote(slot, r);
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[i] += q[i];
+    }
+  }
+}
+
+// fp64 projection of point X by camera (R, t), residual, robust weight and the
+// compact Jacobian (miniba.py:85-132 + 46-54), scaled by sqrt(w).
+template <typename T>
+struct CompactJ {
+  T J0, J1, J2, v0, v1, v2, F0, F1, r0, r1;
+};
+
+template <typename T>
+__device__ __forceinline__ CompactJ<T> linearise(const double* __restrict__ Rm, const double* __restrict__ t,
+                                                 const double X[3], double f, double cx, double cy,
+                                                 double u, double vv, double delta, int loss) {
+  Proj pr = project_residual_fast(Rm, t, X, f, cx, cy, u, vv);
+  const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
+  const double s = sqrt(robust_w(e, delta, loss));
+  CompactJ<T> c;
+  c.r0 = T(s * pr.ru);
+  c.r1 = T(s * pr.rv);
+  if (pr.behind) {  // miniba.py:114,131: rows of behind-camera observations are zeroed
+    c.J0 = c.J1 = c.J2 = c.v0 = c.v1 = c.v2 = c.F0 = c.F1 = T(0);
+    return c;
+  }
+  const double iz = 1.0 / pr.pc[2];
+  const double fz = f * iz;
+  c.J0 = T(s * fz);
+  c.J1 = T(-s * fz * pr.pc[0] * iz);
+  c.J2 = T(-s * fz * pr.pc[1] * iz);
+  c.v0 = T(pr.v[0]);
+  c.v1 = T(pr.v[1]);
+  c.v2 = T(pr.v[2]);
+  c.F0 = T(s * pr.pc[0] * iz);
+  c.F1 = T(s * pr.pc[1] * iz);
+  return c;
+}
+
+// Q = (Jp R) L^-T for one observation: two rows of 3 (forward substitution
+// with the point factor; L diagonal stored inverted).
+template <typename T>
+__device__ __forceinline__ void q_rows(T J0, T J1, T J2, const T (&Rt)[9], const T* __restrict__ L, T q[6]) {
+  const T iL00 = L[0], L10 = L[1], iL11 = L[2], L20 = L[3], L21 = L[4], iL22 = L[5];
+  T b[6];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    b[c] = J0 * Rt[c] + J1 * Rt[6 + c];
+    b[3 + c] = J0 * Rt[3 + c] + J2 * Rt[6 + c];
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const T x0 = b[3 * r] * iL00;
+    const T x1 = (b[3 * r + 1] - L10 * x0) * iL11;
+    const T x2 = (b[3 * r + 2] - L20 * x0 - L21 * x1) * iL22;
+    q[3 * r] = x0;
+    q[3 * r + 1] = x1;
+    q[3 * r + 2] = x2;
+  }
+}
+
+// A = Jp [-[v]x | I] (2x6), rotation columns first (miniba.py:116-128)
+template <typename T>
+__device__ __forceinline__ void expand_A(T J0, T J1, T J2, T v0, T v1, T v2, T a[12]) {
+  a[0] = J1 * v1;
+  a[1] = J0 * v2 - J1 * v0;
+  a[2] = -J0 * v1;
+  a[3] = J0;
+  a[4] = T(0);
+  a[5] = J1;
+  a[6] = J2 * v1 - J0 * v2;
+  a[7] = -J2 * v0;
+  a[8] = J0 * v0;
+  a[9] = T(0);
+  a[10] = J0;
+  a[11] = J2;
+}
+
+// ---------------------------------------------------------------------------
+
+template <typename T, int R>
+__device__ void solve_problem(const Params& P, unsigned char* smem) {
+  using F = Fixed<T>;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int rank = Clu<R>::rank();
+  const int b = (int)(blockIdx.x / R);
+  const bool lead = rank == 0 && tid == 0;
+  const MbaBatchDesc& D = P.d;
+  const MbaLmConfig& cfg = P.cfg;
+  const MbaOutputs& O = P.o;
+
+  double* Rc = (double*)(smem + F::oRc);
+  double* tc = (double*)(smem + F::oTc);
+  double* Rt = (double*)(smem + F::oRt);
+  double* tt = (double*)(smem + F::oTt);
+  double* dc = (double*)(smem + F::oDc);
+  double* xch = (double*)(smem + F::oXch);
+  double* red = (double*)(smem + F::oRed);
+  T* S = (T*)(smem + F::oS);
+  T* job = (T*)(smem + F::oJob);
+  T* jsum = R > 1 ? (T*)(smem + F::oJsum) : job;
+  T* invd = (T*)(smem + F::oInvd);
+  unsigned short* tab = (unsigned short*)(smem + F::oTab);
+  int* cam_ptr = (int*)(smem + F::oCamPtr);
+  int* slot = (int*)(smem + F::oSlot);
+  int* cslot = (int*)(smem + F::oCos);
+  int* blk_off = (int*)(smem + F::oBlkOff);
+  unsigned char* blk_a = smem + F::oBlkA;
+  unsigned char* blk_b = smem + F::oBlkB;
+  unsigned char* arena = smem + F::kBytes;
+
+  __shared__ int s_flag, s_nf, s_nlp, s_npairs, s_job;
+  __shared__ int s_wtot[NW];
+  int epoch = 0;
+
+  const int64_t cb = D.cam_off[b], pb = D.pt_off[b], ob = D.obs_off[b];
+  const int n = (int)(D.cam_off[b + 1] - cb);
+  const int Pn = (int)(D.pt_off[b + 1] - pb);
+  const int K = (int)(D.obs_off[b + 1] - ob);
+  const uint8_t fl = D.flags[b];
+  const bool has_f = fl & 1, opt_pts = (fl >> 1) & 1;
+  const double cx = D.cx[b], cy = D.cy[b];
+  const double delta = cfg.delta, nu = cfg.nu;
+  const int loss = cfg.loss, max_it = cfg.max_iters;
+  const MbaObs* __restrict__ gobs = D.obs + ob;
+  const float* __restrict__ glo = D.obs_lo ? D.obs_lo + 2 * ob : nullptr;
+
+  // ---------------- setup ----------------
+  for (int i = tid; i < n * 9; i += NT) Rc[i] = O.R_in[cb * 9 + i];
+  for (int i = tid; i < n * 3; i += NT) tc[i] = O.t_in[cb * 3 + i];
+  if (tid == 0) {
+    int nf = 0;
+    for (int c = 0; c < n; ++c) {
+      if (D.fixed[cb + c]) {
+        slot[c] = -1;
+      } else {
+        slot[c] = nf;
+        cslot[nf] = c;
+        ++nf;
+      }
+    }
+    int q = 0;
+    for (int a = 0; a < nf; ++a)
+      for (int bb = a; bb < nf; ++bb, ++q) {
+        blk_a[q] = (unsigned char)a;
+        blk_b[q] = (unsigned char)bb;
+      }
+    s_nf = nf;
+    s_flag = (n > MAXN) ? 1 : 0;
+  }
+  // validation of the whole problem (every CTA, so the verdict needs no exchange)
+  for (int k = tid; k < K; k += NT) {
+    const int pt = __ldg(&gobs[k].pt), c = __ldg(&gobs[k].cam);
+    if (pt < 0 || pt >= Pn || c < 0 || c >= n || (k > 0 && __ldg(&gobs[k - 1].pt) > pt)) s_flag = 1;
+  }
+  __syncthreads();
+  const int nf = s_nf, C = 6 * nf + (has_f ? 1 : 0), FI = C - 1, CA = C * (C + 3) / 2;
+  const int nb = opt_pts ? nf * (nf + 1) / 2 : 0;
+  double f = O.focal_in[b];
+  if (s_flag) {  // malformed problem: report and leave parameters untouched
+    if (lead) {
+      O.n_iters[b] = 0;
+      O.status[b] = -1;
+      O.focal_out[b] = f;
+    }
+    if (rank == 0) {
+      for (int i = tid; i < n * 9; i += NT) O.R_out[cb * 9 + i] = O.R_in[cb * 9 + i];
+      for (int i = tid; i < n * 3; i += NT) O.t_out[cb * 3 + i] = O.t_in[cb * 3 + i];
+    }
+    for (int i = rank * NT + tid; i < Pn * 3; i += R * NT)
+      O.points_out[pb * 3 + i] = O.points_in[pb * 3 + i];
+    return;
+  }
+
+  // this CTA's observation slice [k0, k1): point-aligned cut near K r / R
+  auto lower_bound_pt = [&](int p) {
+    int lo_i = 0, hi_i = K;
+    while (lo_i < hi_i) {
+      const int mid = (lo_i + hi_i) >> 1;
+      if (__ldg(&gobs[mid].pt) < p) lo_i = mid + 1; else hi_i = mid;
+    }
+    return lo_i;
+  };
+  int k0 = 0, k1 = K;
+  if (R > 1 && K > 0) {
+    if (rank > 0) k0 = lower_bound_pt(__ldg(&gobs[(int)((int64_t)K * rank / R)].pt));
+    if (rank < R - 1) k1 = lower_bound_pt(__ldg(&gobs[(int)((int64_t)K * (rank + 1) / R)].pt));
+  }
+  const int nlo = k1 - k0;
+  // points [p_lo, p_hi) belong to this rank (unobserved points included: they
+  // keep their value, dp = 0, as in the reference)
+  const int p_lo = rank == 0 ? 0 : (k0 < K ? __ldg(&gobs[k0].pt) : Pn);
+  const int p_hi = rank == R - 1 ? Pn : (k1 < K ? __ldg(&gobs[k1].pt) : Pn);
+  if (O.points_in != O.points_out)
+    for (int i = p_lo * 3 + tid; i < p_hi * 3; i += NT) O.points_out[pb * 3 + i] = O.points_in[pb * 3 + i];
+
+  // count observed points of the slice
+  {
+    int cnt = 0;
+    for (int kl = tid; kl < nlo; kl += NT)
+      cnt += (kl == 0 || __ldg(&gobs[k0 + kl].pt) != __ldg(&gobs[k0 + kl - 1].pt)) ? 1 : 0;
+    double v[1] = {(double)cnt};
+    block_sum_d<1>(v, red);
+    if (tid == 0) s_nlp = (int)v[0];
+    __syncthreads();
+  }
+  const int nlp = s_nlp;
+  // arena layout
+  float4* sobs = (float4*)arena;                                        // [nlo] u, v, cam, point slot
+  double* Xs = (double*)(arena + al16(16 * (size_t)nlo));               // [nlp][3]
+  T* jac = (T*)((unsigned char*)Xs + al16(24 * (size_t)nlp));           // [nlo][JSTR]
+  T* pf = (T*)((unsigned char*)jac + al16(sizeof(T) * JSTR * (size_t)nlo));  // [nlp][PSTR]
+  int* lpt = (int*)((unsigned char*)pf + al16(sizeof(T) * PSTR * (size_t)nlp));  // [nlp]
+  unsigned short* perm = (unsigned short*)((unsigned char*)lpt + al16(4 * (size_t)nlp));  // [nlo]
+  unsigned short* ptr = (unsigned short*)((unsigned char*)perm + al16(2 * (size_t)nlo));  // [nlp+1]
+  unsigned* pairs = (unsigned*)((unsigned char*)ptr + al16(2 * (size_t)(nlp + 1)));
+  const size_t fixed_need = (size_t)((unsigned char*)pairs - arena);
+  bool overflow = fixed_need > P.arena || nlo >= 65535;
+
+  if (!overflow) {
+    // stage observations; slots by a block-wide scan of "first observation of a point"
+    int base = 0;
+    for (int c0 = 0; c0 < nlo; c0 += NT) {
+      const int kl = c0 + tid;
+      int flag = 0, pt = 0;
+      float4 rec = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (kl < nlo) {
+        rec = __ldg(reinterpret_cast<const float4*>(gobs) + k0 + kl);
+        pt = __float_as_int(rec.w);
+        flag = (kl == 0 || __ldg(&gobs[k0 + kl - 1].pt) != pt) ? 1 : 0;
+      }
+      const int inc = warp_incl_scan(flag, lane);
+      if (lane == 31) s_wtot[wid] = inc;
+      __syncthreads();
+      int pre = base;
+      for (int w = 0; w < wid; ++w) pre += s_wtot[w];
+      int tot = 0;
+      for (int w = 0; w < NW; ++w) tot += s_wtot[w];
+      if (kl < nlo) {
+        const int sl = pre + inc - 1;
+        rec.w = __int_as_float(sl);
+        sobs[kl] = rec;
+        if (flag) {
+          lpt[sl] = pt;
+          ptr[sl] = (unsigned short)kl;
+        }
+      }
+      base += tot;
+      __syncthreads();
+    }
+    if (tid == 0) ptr[nlp] = (unsigned short)nlo;
+    __syncthreads();
+    for (int i = tid; i < nlp * 3; i += NT) Xs[i] = O.points_in[(pb + lpt[i / 3]) * 3 + i % 3];
+    // camera-major permutation of the slice (warp per camera, ballot sweeps)
+    for (int c = wid; c < n; c += NW) {
+      int cnt = 0;
+      for (int q0 = 0; q0 < nlo; q0 += 32) {
+        const int q = q0 + lane;
+        cnt += __popc(__ballot_sync(0xffffffffu, q < nlo && __float_as_int(sobs[q].z) == c));
+      }
+      if (lane == 0) cam_ptr[c + 1] = cnt;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      cam_ptr[0] = 0;
+      for (int c = 0; c < n; ++c) cam_ptr[c + 1] += cam_ptr[c];
+    }
+    __syncthreads();
+    for (int c = wid; c < n; c += NW) {
+      int basec = cam_ptr[c];
+      for (int q0 = 0; q0 < nlo; q0 += 32) {
+        const int q = q0 + lane;
+        const bool hit = q < nlo && __float_as_int(sobs[q].z) == c;
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (hit) perm[basec + __popc(m & ((1u << lane) - 1u))] = (unsigned short)q;
+        basec += __popc(m);
+      }
+    }
+    __syncthreads();
+    // co-observation pair lists per free camera block (a <= b): count, scan, fill
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int blk = wid; blk < nb; blk += NW) {
+        const int ca = cslot[blk_a[blk]], cbb = cslot[blk_b[blk]];
+        const int q1 = cam_ptr[ca + 1];
+        int basep = pass ? blk_off[blk] : 0;
+        for (int q0 = cam_ptr[ca]; q0 < q1; q0 += 32) {
+          const int q = q0 + lane;
+          int i = -1, j0 = 0, j1 = 0, m = 0;
+          if (q < q1) {
+            i = perm[q];
+            const int sl = __float_as_int(sobs[i].w);
+            j0 = ptr[sl];
+            j1 = ptr[sl + 1];
+            for (int j = j0; j < j1; ++j) m += __float_as_int(sobs[j].z) == cbb;
+          }
+          if (pass) {
+            const int inc = warp_incl_scan(m, lane);
+            int pos = basep + inc - m;
+            for (int j = j0; j < j1 && m; ++j)
+              if (__float_as_int(sobs[j].z) == cbb) pairs[pos++] = ((unsigned)i << 16) | (unsigned)j;
+          }
+          basep += warp_sum(m);
+        }
+        if (!pass && lane == 0) blk_off[blk + 1] = basep;
+      }
+      __syncthreads();
+      if (!pass) {
+        if (tid == 0) {
+          blk_off[0] = 0;
+          for (int q = 0; q < nb; ++q) blk_off[q + 1] += blk_off[q];
+          s_npairs = blk_off[nb];
+        }
+        __syncthreads();
+        if (fixed_need + 4 * (size_t)s_npairs > P.arena) {
+          overflow = true;
+          break;
+        }
+      }
+    }
+  }
+  // packed position -> (row, col) table of the augmented system
+  for (int j = tid; j < C; j += NT) {
+    const int a0 = acol(j, C);
+    for (int i = j; i <= C; ++i) tab[a0 + i - j] = (unsigned short)((i << 8) | j);
+  }
+  {  // the cluster agrees on overflow (the CTA kernel then re-solves this problem)
+    double v[1] = {overflow ? 1.0 : 0.0};
+    cluster_sum<R, 1>(v, xch, epoch);
+    if (v[0] != 0.0) {
+      if (lead) O.status[b] = kStatusPlanOverflow;
+      Clu<R>::sync();
+      return;
+    }
+  }
+  __syncthreads();
+
+  auto obs_uv = [&](int kl, const float4& o, double& u, double& vv) {
+    u = (double)o.x;
+    vv = (double)o.y;
+    if (glo != nullptr) {
+      const float2 l = __ldg(reinterpret_cast<const float2*>(glo) + k0 + kl);
+      u += (double)l.x;
+      vv += (double)l.y;
+    }
+  };
+
+  // cost pass over the slice with camera set (Rs, ts), focal ft and points
+  // X + frac * dp; cluster-summed (sum rho, sum e, sum e^2)
+  auto cost = [&](const double* Rs, const double* ts, double ft, double frac, bool use_dp, double out[3]) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    constexpr int U = 4;
+    for (int c0 = tid; c0 < nlo; c0 += U * NT) {
+      float4 o[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c0 + u * NT < nlo) o[u] = sobs[c0 + u * NT];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kl = c0 + u * NT;
+        if (kl >= nlo) continue;
+        const int sl = __float_as_int(o[u].w), c = __float_as_int(o[u].z);
+        double Xp[3] = {Xs[3 * sl], Xs[3 * sl + 1], Xs[3 * sl + 2]};
+        if (use_dp) {
+          const T* dp = pf + (size_t)sl * PSTR + 12;
+          Xp[0] = Xp[0] + frac * (double)dp[0];
+          Xp[1] = Xp[1] + frac * (double)dp[1];
+          Xp[2] = Xp[2] + frac * (double)dp[2];
+        }
+        double uu, vv;
+        obs_uv(kl, o[u], uu, vv);
+        Proj pr = project_residual_fast(Rs + 9 * c, ts + 3 * c, Xp, ft, cx, cy, uu, vv);
+        const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
+        acc[0] += robust_rho(e, delta, loss);
+        acc[1] += e;
+        acc[2] += e * e;
+      }
+    }
+    block_sum_d<3>(acc, red);
+    cluster_sum<R, 3>(acc, xch, epoch);
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+  };
+
+  double* costs = O.costs + (size_t)b * (max_it + 1);
+  double* lambdas = O.lambdas + (size_t)b * max_it;
+  uint8_t* accepted = O.accepted + (size_t)b * max_it;
+  uint8_t* evals = O.evals + (size_t)b * max_it;
+
+  // initial cost (miniba.py:232-235)
+  double st[3];
+  cost(Rc, tc, f, 0.0, false, st);
+  double cur = st[0], se = st[1], se2 = st[2];
+  double lam = cfg.lambda_init;
+  if (lead) costs[0] = cur;
+  int it = 0, stop_reason = MBA_SOLVE_MAX_ITERS;
+
+  for (; it < max_it;) {
+    const T tlam = T(lam);
+    // ---------- point pass: compact Jacobians, V_p / g_p / Wf_p, point factor ----------
+    T part[4] = {T(0), T(0), T(0), T(0)};  // U_ff, g_f, sum yf.yf, sum yf.z
+    for (int sl = tid; sl < nlp; sl += NT) {
+      const double Xp[3] = {Xs[3 * sl], Xs[3 * sl + 1], Xs[3 * sl + 2]};
+      T V[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};  // 00 10 11 20 21 22
+      T g[3] = {T(0), T(0), T(0)}, wf[3] = {T(0), T(0), T(0)};
+      const int j0 = ptr[sl], j1 = ptr[sl + 1];
+      for (int kl = j0; kl < j1; ++kl) {
+        const float4 o = sobs[kl];
+        const int c = __float_as_int(o.z);
+        double uu, vv;
+        obs_uv(kl, o, uu, vv);
+        const CompactJ<T> cj = linearise<T>(Rc + 9 * c, tc + 3 * c, Xp, f, cx, cy, uu, vv, delta, loss);
+        T* jk = jac + (size_t)kl * JSTR;
+        jk[0] = cj.J0; jk[1] = cj.J1; jk[2] = cj.J2;
+        jk[3] = cj.v0; jk[4] = cj.v1; jk[5] = cj.v2;
+        jk[6] = cj.F0; jk[7] = cj.F1; jk[8] = cj.r0; jk[9] = cj.r1;
+        if (has_f) {
+          part[0] += cj.F0 * cj.F0 + cj.F1 * cj.F1;
+          part[1] += cj.F0 * cj.r0 + cj.F1 * cj.r1;
+        }
+        if (opt_pts) {
+          const double* Rk = Rc + 9 * c;
+          T B0[3], B1[3];
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            B0[q] = cj.J0 * T(Rk[q]) + cj.J1 * T(Rk[6 + q]);
+            B1[q] = cj.J0 * T(Rk[3 + q]) + cj.J2 * T(Rk[6 + q]);
+          }
+          V[0] += B0[0] * B0[0] + B1[0] * B1[0];
+          V[1] += B0[1] * B0[0] + B1[1] * B1[0];
+          V[2] += B0[1] * B0[1] + B1[1] * B1[1];
+          V[3] += B0[2] * B0[0] + B1[2] * B1[0];
+          V[4] += B0[2] * B0[1] + B1[2] * B1[1];
+          V[5] += B0[2] * B0[2] + B1[2] * B1[2];
+#pragma unroll
+          for (int q = 0; q < 3; ++q) g[q] += B0[q] * cj.r0 + B1[q] * cj.r1;
+          if (has_f)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) wf[q] += B0[q] * cj.F0 + B1[q] * cj.F1;
+        }
+      }
+      if (!opt_pts) continue;
+      // damping (miniba.py:191-193) and 3x3 Cholesky of Vd
+      V[0] += tlam * (V[0] > T(kDiagFloor) ? V[0] : T(kDiagFloor));
+      V[2] += tlam * (V[2] > T(kDiagFloor) ? V[2] : T(kDiagFloor));
+      V[5] += tlam * (V[5] > T(kDiagFloor) ? V[5] : T(kDiagFloor));
+      const T L00 = sqrt(V[0]);
+      const T i00 = T(1) / L00;
+      const T L10 = V[1] * i00, L20 = V[3] * i00;
+      const T L11 = sqrt(V[2] - L10 * L10);
+      const T i11 = T(1) / L11;
+      const T L21 = (V[4] - L20 * L10) * i11;
+      const T L22 = sqrt(V[5] - L20 * L20 - L21 * L21);
+      const T i22 = T(1) / L22;
+      const T z0 = g[0] * i00, z1 = (g[1] - L10 * z0) * i11, z2 = (g[2] - L20 * z0 - L21 * z1) * i22;
+      const T f0 = wf[0] * i00, f1 = (wf[1] - L10 * f0) * i11, f2 = (wf[2] - L20 * f0 - L21 * f1) * i22;
+      part[2] += f0 * f0 + f1 * f1 + f2 * f2;
+      part[3] += f0 * z0 + f1 * z1 + f2 * z2;
+      T* pw = pf + (size_t)sl * PSTR;
+      pw[0] = i00; pw[1] = L10; pw[2] = i11; pw[3] = L20; pw[4] = L21; pw[5] = i22;
+      pw[6] = z0; pw[7] = z1; pw[8] = z2;
+      pw[9] = f0; pw[10] = f1; pw[11] = f2;
+    }
+    {  // this CTA's focal partials
+      double pd[4] = {(double)part[0], (double)part[1], (double)part[2], (double)part[3]};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pd[i] = (double)warp_sum(part[i]);
+      if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) red[wid * 4 + i] = pd[i];
+      if (tid == 0) s_job = 0;
+      __syncthreads();
+      if (tid < 4) {
+        T s_ = T(0);
+        for (int w = 0; w < NW; ++w) s_ += T(red[w * 4 + tid]);
+        job[JOB_PART + tid] = s_;
+      }
+    }
+
+    // ---------- camera jobs + pair jobs (warps pull jobs from a queue) ----------
+    for (;;) {
+      int jb = 0;
+      if (lane == 0) jb = atomicAdd(&s_job, 1);
+      jb = __shfl_sync(0xffffffffu, jb, 0);
+      if (jb >= nf + nb) break;
+      if (jb < nf) {
+        const int s = jb, c = cslot[s];
+        T Rt9[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) Rt9[i] = T(Rc[9 * c + i]);
+        T acc[UST];
+#pragma unroll
+        for (int i = 0; i < UST; ++i) acc[i] = T(0);
+        for (int q = cam_ptr[c] + lane; q < cam_ptr[c + 1]; q += 32) {
+          const int kl = perm[q];
+          const T* jk = jac + (size_t)kl * JSTR;
+          const T J0 = jk[0], J1 = jk[1], J2 = jk[2], F0 = jk[6], F1 = jk[7], r0 = jk[8], r1 = jk[9];
+          T a[12];
+          expand_A(J0, J1, J2, jk[3], jk[4], jk[5], a);
+          int idx = 0;
+#pragma unroll
+          for (int r = 0; r < 6; ++r) {
+#pragma unroll
+            for (int cc = 0; cc <= r; ++cc) acc[idx++] += a[r] * a[cc] + a[6 + r] * a[6 + cc];
+            acc[21 + r] += a[r] * F0 + a[6 + r] * F1;
+            acc[27 + r] += a[r] * r0 + a[6 + r] * r1;
+          }
+          if (opt_pts) {
+            const int sl = __float_as_int(sobs[kl].w);
+            const T* pw = pf + (size_t)sl * PSTR;
+            T qv[6];
+            q_rows(J0, J1, J2, Rt9, pw, qv);
+            const T qf0 = qv[0] * pw[9] + qv[1] * pw[10] + qv[2] * pw[11];
+            const T qf1 = qv[3] * pw[9] + qv[4] * pw[10] + qv[5] * pw[11];
+            const T qz0 = qv[0] * pw[6] + qv[1] * pw[7] + qv[2] * pw[8];
+            const T qz1 = qv[3] * pw[6] + qv[4] * pw[7] + qv[5] * pw[8];
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+              acc[33 + r] += a[r] * qf0 + a[6 + r] * qf1;
+              acc[39 + r] += a[r] * qz0 + a[6 + r] * qz1;
+            }
+          }
+        }
+        warp_reduce_to<T, UST>(acc, job + s * UST, lane);
+      } else {
+        const int blk = jb - nf;
+        const int ca = cslot[blk_a[blk]], cbb = cslot[blk_b[blk]];
+        T Ra[9], Rb[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          Ra[i] = T(Rc[9 * ca + i]);
+          Rb[i] = T(Rc[9 * cbb + i]);
+        }
+        T acc[36];
+#pragma unroll
+        for (int i = 0; i < 36; ++i) acc[i] = T(0);
+        const int q1 = blk_off[blk + 1];
+        for (int q = blk_off[blk] + lane; q < q1; q += 32) {
+          const unsigned pr = pairs[q];
+          const int i = (int)(pr >> 16), j = (int)(pr & 0xffffu);
+          const T* pw = pf + (size_t)__float_as_int(sobs[i].w) * PSTR;
+          const T* ji = jac + (size_t)i * JSTR;
+          const T* jj = jac + (size_t)j * JSTR;
+          const T Ji0 = ji[0], Ji1 = ji[1], Ji2 = ji[2], vi0 = ji[3], vi1 = ji[4], vi2 = ji[5];
+          const T Jj0 = jj[0], Jj1 = jj[1], Jj2 = jj[2], vj0 = jj[3], vj1 = jj[4], vj2 = jj[5];
+          T qi[6], qj[6];
+          q_rows(Ji0, Ji1, Ji2, Ra, pw, qi);
+          q_rows(Jj0, Jj1, Jj2, Rb, pw, qj);
+          // M = Q_i Q_j^T (2x2)
+          const T m00 = qi[0] * qj[0] + qi[1] * qj[1] + qi[2] * qj[2];
+          const T m01 = qi[0] * qj[3] + qi[1] * qj[4] + qi[2] * qj[5];
+          const T m10 = qi[3] * qj[0] + qi[4] * qj[1] + qi[5] * qj[2];
+          const T m11 = qi[3] * qj[3] + qi[4] * qj[4] + qi[5] * qj[5];
+          // N = M Jp_j (2x3), M3 = Jp_i^T N (3x3)
+          const T n00 = m00 * Jj0, n01 = m01 * Jj0, n02 = m00 * Jj1 + m01 * Jj2;
+          const T n10 = m10 * Jj0, n11 = m11 * Jj0, n12 = m10 * Jj1 + m11 * Jj2;
+          T M3[9];
+          M3[0] = Ji0 * n00; M3[1] = Ji0 * n01; M3[2] = Ji0 * n02;
+          M3[3] = Ji0 * n10; M3[4] = Ji0 * n11; M3[5] = Ji0 * n12;
+          M3[6] = Ji1 * n00 + Ji2 * n10; M3[7] = Ji1 * n01 + Ji2 * n11; M3[8] = Ji1 * n02 + Ji2 * n12;
+          // H = M3 G_j = [E | M3], E row r = -(M3 row r) x v_j
+          T H[18];  // row-major 3x6
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            const T a0 = M3[3 * r], a1 = M3[3 * r + 1], a2 = M3[3 * r + 2];
+            H[6 * r + 0] = a2 * vj1 - a1 * vj2;
+            H[6 * r + 1] = a0 * vj2 - a2 * vj0;
+            H[6 * r + 2] = a1 * vj0 - a0 * vj1;
+            H[6 * r + 3] = a0;
+            H[6 * r + 4] = a1;
+            H[6 * r + 5] = a2;
+          }
+          // block = G_i^T H = [[v_i]x H ; H]
+#pragma unroll
+          for (int cc = 0; cc < 6; ++cc) {
+            const T h0 = H[cc], h1 = H[6 + cc], h2 = H[12 + cc];
+            acc[0 * 6 + cc] += vi1 * h2 - vi2 * h1;
+            acc[1 * 6 + cc] += vi2 * h0 - vi0 * h2;
+            acc[2 * 6 + cc] += vi0 * h1 - vi1 * h0;
+            acc[3 * 6 + cc] += h0;
+            acc[4 * 6 + cc] += h1;
+            acc[5 * 6 + cc] += h2;
+          }
+        }
+        warp_reduce_to<T, 36>(acc, job + JOB_PAIR0 + blk * 36, lane);
+      }
+    }
+    Clu<R>::sync();  // every CTA's job outputs are complete and visible
+    if constexpr (R > 1) {
+      const T* rj[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) rj[r] = Clu<R>::remote(job, r);
+      for (int i = tid; i < JOB_OUT; i += NT) {
+        T s_ = T(0);
+#pragma unroll
+        for (int r = 0; r < R; ++r) s_ += rj[r][i];
+        jsum[i] = s_;
+      }
+      __syncthreads();
+    }
+
+    // ---------- assemble the damped augmented reduced system (miniba.py:188-213) ----------
+    for (int e = tid; e < CA; e += NT) {
+      const unsigned ij = tab[e];
+      const int i = (int)(ij >> 8), j = (int)(ij & 255u);
+      T val;
+      if (i == C) {                       // rhs row
+        if (j == FI && has_f) {
+          val = -jsum[JOB_PART + 1] + (opt_pts ? jsum[JOB_PART + 3] : T(0));
+        } else {
+          const T* u = jsum + (j / 6) * UST;
+          val = -u[27 + j % 6] + (opt_pts ? u[39 + j % 6] : T(0));
+        }
+      } else if (has_f && i == FI) {      // focal row
+        if (j == FI) {
+          const T uff = jsum[JOB_PART + 0];
+          val = uff + tlam * (uff > T(kDiagFloor) ? uff : T(kDiagFloor)) -
+                (opt_pts ? jsum[JOB_PART + 2] : T(0));
+        } else {
+          const T* u = jsum + (j / 6) * UST;
+          val = u[21 + j % 6] - (opt_pts ? u[33 + j % 6] : T(0));
+        }
+      } else {                            // camera-camera: i >= j
+        const int sb = i / 6, sa = j / 6, ri = i % 6, rj = j % 6;
+        T schur = T(0);
+        val = T(0);
+        if (sa == sb) {
+          const int r = ri, cc = rj;  // r >= cc
+          T ud = jsum[sa * UST + r * (r + 1) / 2 + cc];
+          if (r == cc) ud += tlam * (ud > T(kDiagFloor) ? ud : T(kDiagFloor));
+          val = ud;
+          if (opt_pts) {
+            const int q = sa * nf - sa * (sa - 1) / 2;   // block (sa, sa)
+            schur = jsum[JOB_PAIR0 + q * 36 + r * 6 + cc];
+          }
+        } else if (opt_pts) {
+          const int q = sa * nf - sa * (sa - 1) / 2 + (sb - sa);   // block (sa, sb)
+          schur = jsum[JOB_PAIR0 + q * 36 + rj * 6 + ri];
+        }
+        val -= schur;
+      }
+      S[e] = val;
+    }
+    __syncthreads();
+
+    // ---------- LDL^T of the augmented system, one barrier per column ----------
+    bool chol_fail = false;
+    for (int k = 0; k < C; ++k) {
+      const T* colk = S + acol(k, C) - k;  // colk[i] = S[i][k], i in [k, C]
+      const T d = colk[k];
+      if (!(d > T(0)) || !isfinite((double)d)) {
+        chol_fail = true;  // uniform: every thread reads the same pivot
+        break;
+      }
+      const T inv = T(1) / d;
+      if (tid == 0) invd[k] = inv;
+      for (int e = acol(k + 1, C) + tid; e < CA; e += NT) {
+        const unsigned ij = tab[e];
+        S[e] -= colk[ij >> 8] * colk[ij & 255u] * inv;
+      }
+      __syncthreads();
+    }
+    if (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull)) chol_fail = true;
+
+    if (!chol_fail) {
+      // column-oriented back substitution D L^T x = y in warp 0 (no reductions):
+      // x_k = u_k / d_k, then u_j -= S[k][j] x_k for j < k
+      if (wid == 0) {
+        T u0 = lane < C ? S[acol(lane, C) + C - lane] : T(0);
+        T u1 = lane + 32 < C ? S[acol(lane + 32, C) + C - lane - 32] : T(0);
+        for (int k = C - 1; k >= 0; --k) {
+          const T uk = __shfl_sync(0xffffffffu, k < 32 ? u0 : u1, k & 31);
+          const T xk = uk * invd[k];
+          if (lane == (k & 31)) {
+            if (k < 32) u0 = xk; else u1 = xk;
+          }
+          if (lane < k) u0 -= S[acol(lane, C) + k - lane] * xk;
+          if (lane + 32 < k) u1 -= S[acol(lane + 32, C) + k - lane - 32] * xk;
+        }
+        if (lane < C) dc[lane] = (double)u0;
+        if (lane + 32 < C) dc[lane + 32] = (double)u1;
+      }
+      __syncthreads();
+      // point back substitution (miniba.py:216-217): dp = -L^-T (z + yf df + sum Y_i^T dc_a)
+      if (opt_pts) {
+        const T df = has_f ? T(dc[FI]) : T(0);
+        for (int sl = tid; sl < nlp; sl += NT) {
+          T* pw = pf + (size_t)sl * PSTR;
+          T u0 = pw[6] + pw[9] * df, u1 = pw[7] + pw[10] * df, u2 = pw[8] + pw[11] * df;
+          for (int kl = ptr[sl]; kl < ptr[sl + 1]; ++kl) {
+            const int c = __float_as_int(sobs[kl].z);
+            const int s = slot[c];
+            if (s < 0) continue;
+            const T* jk = jac + (size_t)kl * JSTR;
+            const T J0 = jk[0], J1 = jk[1], J2 = jk[2], v0 = jk[3], v1 = jk[4], v2 = jk[5];
+            const T w0 = T(dc[6 * s]), w1 = T(dc[6 * s + 1]), w2 = T(dc[6 * s + 2]);
+            // G dc = -(v x w) + dt ; A dc = Jp (G dc)
+            const T g0 = -(v1 * w2 - v2 * w1) + T(dc[6 * s + 3]);
+            const T g1 = -(v2 * w0 - v0 * w2) + T(dc[6 * s + 4]);
+            const T g2 = -(v0 * w1 - v1 * w0) + T(dc[6 * s + 5]);
+            const T ad0 = J0 * g0 + J1 * g2, ad1 = J0 * g1 + J2 * g2;
+            T Rt9[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) Rt9[i] = T(Rc[9 * c + i]);
+            T qv[6];
+            q_rows(J0, J1, J2, Rt9, pw, qv);
+            u0 += qv[0] * ad0 + qv[3] * ad1;
+            u1 += qv[1] * ad0 + qv[4] * ad1;
+            u2 += qv[2] * ad0 + qv[5] * ad1;
+          }
+          const T iL00 = pw[0], L10 = pw[1], iL11 = pw[2], L20 = pw[3], L21 = pw[4], iL22 = pw[5];
+          const T x2 = u2 * iL22;
+          const T x1 = (u1 - L21 * x2) * iL11;
+          const T x0 = (u0 - L10 * x1 - L20 * x2) * iL00;
+          pw[12] = -x0;
+          pw[13] = -x1;
+          pw[14] = -x2;
+        }
+      }
+    }
+
+    // ---------- trials, accept / reject, lambda (miniba.py:244-293) ----------
+    if (lead) lambdas[it] = lam;
+    int tries = 0, took = -1;
+    double tc_[3] = {0, 0, 0};
+    double ft = f;
+    if (!chol_fail) {
+      for (int q = tid; q < kBacktrackTries * n; q += NT) {
+        const int bt = q / n, c = q % n, s = slot[c];
+        const double frac = ldexp(1.0, -bt);
+        double* Rq = Rt + (size_t)(bt * n + c) * 9;
+        double* tq = tt + (size_t)(bt * n + c) * 3;
+        if (s < 0) {
+          for (int i = 0; i < 9; ++i) Rq[i] = Rc[9 * c + i];
+          for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i];
+        } else {
+          double w[3] = {frac * dc[6 * s], frac * dc[6 * s + 1], frac * dc[6 * s + 2]};
+          double E[9];
+          exp_so3(w, E);
+          matmul33(E, Rc + 9 * c, Rq);
+          for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i] + frac * dc[6 * s + 3 + i];
+        }
+      }
+      __syncthreads();
+      for (int bt = 0; bt < kBacktrackTries; ++bt) {
+        const double frac = ldexp(1.0, -bt);
+        ft = has_f ? f + frac * dc[FI] : f;
+        cost(Rt + (size_t)bt * n * 9, tt + (size_t)bt * n * 3, ft, frac, opt_pts, tc_);
+        ++tries;
+        if (tc_[0] < cur && isfinite(tc_[0])) {
+          took = bt;
+          break;
+        }
+      }
+    } else {
+      Clu<R>::sync();  // job buffers are rewritten next iteration: peers must be done reading
+    }
+    if (lead) evals[it] = (uint8_t)tries;
+    bool stop = false;
+    if (took >= 0) {
+      const double frac = ldexp(1.0, -took);
+      for (int i = tid; i < n * 9; i += NT) Rc[i] = Rt[(size_t)took * n * 9 + i];
+      for (int i = tid; i < n * 3; i += NT) tc[i] = tt[(size_t)took * n * 3 + i];
+      if (opt_pts)
+        for (int i = tid; i < nlp * 3; i += NT) {
+          const T* dp = pf + (size_t)(i / 3) * PSTR + 12;
+          Xs[i] = Xs[i] + frac * (double)dp[i % 3];
+        }
+      f = ft;
+      lam = took == 0 ? fmax(lam / nu, 1e-15) : fmin(lam * nu, kLambdaMax);
+      const double improve = cur - tc_[0];
+      cur = tc_[0];
+      se = tc_[1];
+      se2 = tc_[2];
+      if (lead) accepted[it] = 1;
+      if (improve <= 1e-15 * fmax(cur, 1.0)) {
+        stop = true;
+        stop_reason = MBA_SOLVE_CONVERGED;
+      }
+    } else {
+      lam = fmin(lam * nu, kLambdaMax);
+      if (lead) accepted[it] = 0;
+      if (!chol_fail && lam >= kLambdaMax) {
+        stop = true;
+        stop_reason = MBA_SOLVE_LAMBDA_CAP;
+      }
+    }
+    if (lead) costs[it + 1] = cur;
+    ++it;
+    __syncthreads();
+    if (stop) break;
+  }
+
+  // ---------------- outputs ----------------
+  for (int i = tid; i < nlp * 3; i += NT) O.points_out[(pb + lpt[i / 3]) * 3 + i % 3] = Xs[i];
+  if (rank == 0) {
+    for (int i = tid; i < n * 9; i += NT) O.R_out[cb * 9 + i] = Rc[i];
+    for (int i = tid; i < n * 3; i += NT) O.t_out[cb * 3 + i] = tc[i];
+  }
+  if (lead) {
+    O.focal_out[b] = f;
+    O.n_iters[b] = it;
+    O.status[b] = stop_reason;
+    O.final_stats[4 * b + 0] = cur;
+    O.final_stats[4 * b + 1] = se;
+    O.final_stats[4 * b + 2] = se2;
+    O.final_stats[4 * b + 3] = (double)K;
+  }
+  Clu<R>::sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
+template <typename T, int R, int MINB>
+__global__ void __launch_bounds__(NT, MINB) solve_v4_kernel(Params P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  solve_problem<T, R>(P, smem);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+template <typename T>
+static size_t need_bytes(const MbaBatchDesc* d, int R) {
+  const int64_t mt = d->max_track > 0 ? d->max_track : d->max_obs;
+  const int64_t obs = (d->max_obs + R - 1) / R + mt;
+  const int64_t pts = (d->max_points + R - 1) / R + mt;
+  const int64_t prs = (d->max_pairs + R - 1) / R + mt * mt;
+  return Fixed<T>::kBytes + obs * obs_bytes<T>() + pts * pt_bytes<T>() + 4 * prs + 8 * 16;
+}
+
+template <typename T>
+static int plan_t(const MbaBatchDesc* d) {
+  if (const char* e = getenv("MBA_V4_R")) {
+    const int r = atoi(e);
+    if (r == 1 || r == 2 || r == 4 || r == 8 || r == 16) return need_bytes<T>(d, r) <= kSmemLimit ? r : 0;
+  }
+  for (int R : {1, 2, 4, 8, 16})
+    if (need_bytes<T>(d, R) <= kSmemLimit) return R;
+  return 0;
+}
+
+int plan_cluster(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
+  if (d->max_cams > MAXN || d->max_cams < 1 || d->max_obs >= 65535 * 16) return 0;
+  return cfg->precision == MBA_LIN_F64 ? plan_t<double>(d) : plan_t<float>(d);
+}
+
+template <typename T, int R, int MINB>
+static int launch_t(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st) {
+  auto kern = solve_v4_kernel<T, R, MINB>;
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return MBA_ERR_CUDA;
+  size_t smem = need_bytes<T>(d, R);
+  const size_t cap = kSmemLimit - fa.sharedSizeBytes;
+  if (smem > cap) return MBA_ERR_TOO_LARGE;
+  // take all the shared memory a CTA gets at this occupancy (slack for
+  // unbalanced slices before the overflow fallback triggers); 228 KB per SM,
+  // 1 KB reserved per CTA
+  size_t per = (228 * 1024) / (size_t)MINB - 1024 - fa.sharedSizeBytes;
+  if (per > cap) per = cap;
+  if (smem < per) smem = per;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    if (getenv("MBA_DEBUG")) fprintf(stderr, "mba v4 smem attribute %zu rejected\n", smem);
+    return MBA_ERR_CUDA;
+  }
+  if (R > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  Params P;
+  P.d = *d;
+  P.cfg = *cfg;
+  P.o = *o;
+  P.arena = smem - Fixed<T>::kBytes;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)d->n_problems * R);
+  lc.blockDim = dim3(NT);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = R;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  const cudaError_t err = cudaLaunchKernelEx(&lc, kern, P);
+  if (err != cudaSuccess && getenv("MBA_DEBUG"))
+    fprintf(stderr, "mba v4 launch (R=%d, smem=%zu): %s\n", R, smem, cudaGetErrorString(err));
+  return err == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
+}
+
+template <typename T>
+static int launch_prec(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st,
+                       int R) {
+  constexpr int MB = sizeof(T) == 4 ? 2 : 1;
+  switch (R) {
+    case 1: return need_bytes<T>(d, 1) * 2 + 2048 <= kSmemLimit ? launch_t<T, 1, 2>(d, cfg, o, st)
+                                                                : launch_t<T, 1, 1>(d, cfg, o, st);
+    case 2: return need_bytes<T>(d, 2) * 2 + 2048 <= kSmemLimit ? launch_t<T, 2, 2>(d, cfg, o, st)
+                                                                : launch_t<T, 2, 1>(d, cfg, o, st);
+    case 4: return launch_t<T, 4, MB>(d, cfg, o, st);
+    case 8: return launch_t<T, 8, 1>(d, cfg, o, st);
+    case 16: return launch_t<T, 16, 1>(d, cfg, o, st);
+    default: return MBA_ERR_TOO_LARGE;
+  }
+}
+
+int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st, int R) {
+  if (cfg->precision == MBA_LIN_F64) return launch_prec<double>(d, cfg, o, st, R);
+  return launch_prec<float>(d, cfg, o, st, R);
+}
+
+}  // namespace v4
+}  // namespace mba

@@ -262,7 +262,7 @@ def descriptors(db: DeviceBatch, prm: LmParams, sol: Solution):
     c = MbaLmConfig(lambda_init=prm.lambda_init, nu=prm.nu, delta=prm.delta,
                     max_iters=prm.max_iters, loss=_lib.LOSS[prm.loss],
                     precision=_lib.PRECISION[prm.precision],
-                    ctas_per_problem={"auto": 0, "warp": -1, "cta": -2, "pw": -3, "grid": -4}[prm.kernel],
+                    ctas_per_problem={"auto": 0, "warp": -1, "cta": -2, "pw": -3, "grid": -4, "cta2": -5, "cta128x4": -6, "cta128x3": -7, "cta64": -8, "v4": -9}[prm.kernel],
                     fail_iters_mask=sum(1 << int(i) for i in prm.fail_at if 0 <= int(i) < 64))
     o = MbaOutputs(R_in=ptr(db.R), t_in=ptr(db.t), focal_in=ptr(db.focal), points_in=ptr(db.points),
                    R_out=ptr(sol.R), t_out=ptr(sol.t), focal_out=ptr(sol.focal),

@@ -12,7 +12,7 @@ from oracle import miniba_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "grid"])
+@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "grid", "v4"])
 @pytest.mark.parametrize("path", golden_cases(), ids=golden_ids())
 def test_solver_matches_reference_golden(path, kernel, cuda_ok):
     """float64 mode (the API default): exact trace parity through i* (fp64
@@ -63,7 +63,7 @@ def test_mixed_precision_against_golden(path, cuda_ok):
         assert np.abs(t - out["t"]).max() <= 1e-3 * scale
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp", "pw"])
+@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "v4"])
 @pytest.mark.parametrize("precision", ["mixed", "f64"])
 def test_batched_matches_oracle_and_is_shard_invariant(precision, kernel, cuda_ok):
     from paper_2506_05558_b200.synth import make_batch
@@ -124,7 +124,7 @@ def test_cauchy_outliers_many_cameras(kernel, cuda_ok):
                   p["focal"], label="cauchy16")
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "grid"])
+@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "grid", "v4"])
 def test_fault_injection_matches_oracle(kernel, cuda_ok):
     from paper_2506_05558_b200.synth import make_batch
     p = make_batch(1, n_cams=8, K=2000, seed=4).problem(0)
@@ -149,7 +149,7 @@ def test_max_iters_zero_and_one(cuda_ok):
     np.testing.assert_allclose(d1["costs"], ref["costs"], rtol=1e-9)
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp", "pw"])
+@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "v4"])
 def test_all_cameras_fixed_focal_only(kernel, cuda_ok):
     """C = 1 (focal only) edge shape."""
     from paper_2506_05558_b200.synth import make_batch
@@ -161,7 +161,7 @@ def test_all_cameras_fixed_focal_only(kernel, cuda_ok):
     assert dev["accepted"][:3].tolist() == ref["accepted"][:3].tolist()
 
 
-@pytest.mark.parametrize("other", ["warp", "pw", "grid"])
+@pytest.mark.parametrize("other", ["warp", "pw", "grid", "v4"])
 def test_kernels_agree(other, cuda_ok):
     """All kernels implement the same arithmetic per problem up to reduction
     order: traces agree through i* and final costs to 1e-9 on 64 problems."""
