@@ -2423,6 +2423,7 @@ int32_t mba_abi_version(void) { return MBA_ABI_VERSION; }
 
 #ifdef MBA_PHASE_PROF
 int32_t mba_debug_set_phase_buffer(unsigned long long* dev_buf) {
+  mba::v4::set_prof(dev_buf);
   return cudaMemcpyToSymbol(mba::g_prof, &dev_buf, sizeof(dev_buf)) == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
 }
 #endif

@@ -40,6 +40,7 @@
 #include <stdlib.h>
 
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "mba_common.cuh"
 #include "mba_v4.cuh"
@@ -49,13 +50,21 @@ namespace cg = cooperative_groups;
 namespace mba {
 namespace v4 {
 
-constexpr int NT = 256;
-constexpr int NW = NT / 32;
+constexpr int NW_MAX = 8;                        // layout bound: warps per CTA
+#ifndef MBA_NWF_LDL
+#define MBA_NWF_LDL 2
+#endif
+constexpr int NWF_LDL = MBA_NWF_LDL;   // warps in the reduced-system factorisation
 constexpr int MAXN = 8;                          // cameras per problem
 constexpr int MAXC = 6 * MAXN + 1;               // reduced system size (+ focal)
 constexpr int MAXNB = MAXN * (MAXN + 1) / 2;     // camera blocks a <= b
 constexpr int CA_MAX = MAXC * (MAXC + 3) / 2;    // augmented packed size
-constexpr int JSTR = 11;   // per observation: J0 J1 J2 v0 v1 v2 F0 F1 r0 r1 (+pad, odd stride)
+// per observation: sqrt(w) (f/z, -fx/z^2, -fy/z^2) [+ sqrt(w) r in fp32 mode, where
+// re-deriving the residual from rounded factors would cancel]; v = R X, the
+// focal derivative and (fp64) the residual are recomputed where used. Odd
+// strides keep shared-memory accesses conflict-free.
+template <typename T>
+__host__ __device__ constexpr int jstr() { return sizeof(T) == 8 ? 3 : 5; }
 constexpr int PSTR = 15;   // per point: iL00 L10 iL11 L20 L21 iL22 z0..2 yf0..2 dp0..2
 constexpr int UST = 45;    // camera job: U_aa(21) U_af(6) g_a(6) SYf(6) SYz(6)
 constexpr int JOB_PAIR0 = MAXN * UST;
@@ -74,11 +83,10 @@ struct Fixed {
   static constexpr size_t oTt = oRt + 8 * 9 * MAXN * kBacktrackTries; // double[5][MAXN][3]
   static constexpr size_t oDc = oTt + 8 * 3 * MAXN * kBacktrackTries; // double[MAXC]
   static constexpr size_t oXch = oDc + 8 * MAXC;                      // double[2][4] cluster exchange
-  static constexpr size_t oRed = oXch + 8 * 8;                        // double[NW][4]
-  static constexpr size_t oS = al16(oRed + 8 * NW * 4);               // T[CA_MAX]
+  static constexpr size_t oRed = oXch + 8 * 8;                        // double[NW_MAX][4]
+  static constexpr size_t oS = al16(oRed + 8 * NW_MAX * 4);           // T[CA_MAX]
   static constexpr size_t oJob = al16(oS + sizeof(T) * CA_MAX);       // T[JOB_OUT] this CTA's partials
-  static constexpr size_t oJsum = al16(oJob + sizeof(T) * JOB_OUT);   // T[JOB_OUT] cluster sums
-  static constexpr size_t oInvd = al16(oJsum + sizeof(T) * JOB_OUT);  // T[MAXC]
+  static constexpr size_t oInvd = al16(oJob + sizeof(T) * JOB_OUT);   // T[MAXC]
   static constexpr size_t oTab = al16(oInvd + sizeof(T) * MAXC);      // u16[CA_MAX] (row<<8|col)
   static constexpr size_t oCamPtr = al16(oTab + 2 * CA_MAX);          // int[MAXN+1]
   static constexpr size_t oSlot = oCamPtr + 4 * (MAXN + 1);           // int[MAXN]
@@ -86,14 +94,32 @@ struct Fixed {
   static constexpr size_t oBlkOff = oCos + 4 * MAXN;                  // int[MAXNB+1]
   static constexpr size_t oBlkA = oBlkOff + 4 * (MAXNB + 1);          // u8[MAXNB]
   static constexpr size_t oBlkB = oBlkA + MAXNB;                      // u8[MAXNB]
-  static constexpr size_t kBytes = al16(oBlkB + MAXNB);
+  static constexpr size_t oRcT = al16(oBlkB + MAXNB);                 // T[MAXN][9] rotations in T
+  static constexpr size_t oDcT = al16(oRcT + sizeof(T) * 9 * MAXN);   // T[MAXC] step in T
+  static constexpr size_t kBytes = al16(oDcT + sizeof(T) * MAXC);
 };
 
 // bytes per local observation / observed point in the arena (plus pairs, 4 B each)
 template <typename T>
-__host__ __device__ constexpr size_t obs_bytes() { return 16 + sizeof(T) * JSTR + 2; }
+__host__ __device__ constexpr size_t obs_bytes() { return 16 + sizeof(T) * jstr<T>() + 2; }
 template <typename T>
 __host__ __device__ constexpr size_t pt_bytes() { return 24 + sizeof(T) * PSTR + 4 + 2; }
+
+// Optional per-phase cycle counters (-DMBA_PHASE_PROF, scripts/phase_prof.py):
+// thread 0 of every CTA accumulates clock64() deltas between phase marks.
+enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_CHA, PH_CHB, PH_N };
+#ifdef MBA_PHASE_PROF
+__device__ unsigned long long* g_prof = nullptr;
+#define PROF_DECL __shared__ long long s_prof[PH_N]; long long prof_t = clock64(); \
+  if (threadIdx.x == 0) for (int i = 0; i < PH_N; ++i) s_prof[i] = 0;
+#define PROF_MARK(ph) if (threadIdx.x == 0) { long long now = clock64(); s_prof[ph] += now - prof_t; prof_t = now; }
+#define PROF_FLUSH if (threadIdx.x == 0 && g_prof) for (int i = 0; i < PH_N; ++i) atomicAdd(g_prof + i, (unsigned long long)s_prof[i]);
+void set_prof(unsigned long long* p) { cudaMemcpyToSymbol(g_prof, &p, sizeof(p)); }
+#else
+#define PROF_DECL
+#define PROF_MARK(ph)
+#define PROF_FLUSH
+#endif
 
 struct Params {
   MbaBatchDesc d;
@@ -158,7 +184,7 @@ __device__ __forceinline__ void warp_reduce_to(T (&v)[N], T* out, int lane) {
 }
 
 // Deterministic block sum of N doubles (result to every thread).
-template <int N>
+template <int NW, int N>
 __device__ __forceinline__ void block_sum_d(double (&v)[N], double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -217,6 +243,46 @@ __device__ __forceinline__ void cluster_sum(double (&v)[N], double* xch, int& ep
   }
 }
 
+// fp64 projection with the reciprocal depth kept (miniba.py:85-98; one
+// reciprocal instead of two divisions, <= 1 ulp from the reference's (f x)/z)
+struct ProjZ {
+  double pc[3], v[3], ru, rv, iz;
+  bool behind;
+};
+__device__ __forceinline__ ProjZ proj_z(const double* __restrict__ R, const double* __restrict__ t,
+                                        const double X[3], double f, double cx, double cy, double u,
+                                        double vv) {
+  ProjZ o;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    o.pc[i] = R[i * 3 + 0] * X[0] + R[i * 3 + 1] * X[1] + R[i * 3 + 2] * X[2] + t[i];
+    o.v[i] = o.pc[i] - t[i];  // R X recovered as p_cam - t, as miniba.py:117 does
+  }
+  o.behind = !(o.pc[2] > kZMin);
+  o.iz = 1.0 / (o.behind ? kZMin : o.pc[2]);
+  o.ru = o.behind ? kBadResidual : f * o.pc[0] * o.iz + cx - u;
+  o.rv = o.behind ? kBadResidual : f * o.pc[1] * o.iz + cy - vv;
+  return o;
+}
+
+// robust cost from the squared residual norm (miniba.py:46-50 + Cauchy): the
+// square root is only taken for Huber observations beyond delta
+__device__ __forceinline__ double rho_e2(double e2, double delta, int loss) {
+  if (loss == MBA_LOSS_CAUCHY) return 0.5 * delta * delta * log1p(e2 / (delta * delta));
+  if (e2 <= delta * delta) return 0.5 * e2;
+  const double e = sqrt(e2);
+  return e <= delta ? 0.5 * e * e : delta * (e - 0.5 * delta);
+}
+
+// sqrt of the IRLS weight (miniba.py:52-54 + Cauchy). e2 <= delta^2 implies
+// sqrt(e2) <= delta after rounding, so inliers need no square root at all.
+__device__ __forceinline__ double sqrt_w_e2(double e2, double delta, int loss) {
+  if (loss == MBA_LOSS_CAUCHY) return sqrt(1.0 / (1.0 + e2 / (delta * delta)));
+  if (e2 <= delta * delta) return 1.0;
+  const double e = sqrt(e2);
+  return e <= delta ? 1.0 : sqrt(delta / fmax(e, 1e-300));
+}
+
 // fp64 projection of point X by camera (R, t), residual, robust weight and the
 // compact Jacobian (miniba.py:85-132 + 46-54), scaled by sqrt(w).
 template <typename T>
@@ -228,9 +294,8 @@ template <typename T>
 __device__ __forceinline__ CompactJ<T> linearise(const double* __restrict__ Rm, const double* __restrict__ t,
                                                  const double X[3], double f, double cx, double cy,
                                                  double u, double vv, double delta, int loss) {
-  Proj pr = project_residual_fast(Rm, t, X, f, cx, cy, u, vv);
-  const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
-  const double s = sqrt(robust_w(e, delta, loss));
+  const ProjZ pr = proj_z(Rm, t, X, f, cx, cy, u, vv);
+  const double s = sqrt_w_e2(pr.ru * pr.ru + pr.rv * pr.rv, delta, loss);
   CompactJ<T> c;
   c.r0 = T(s * pr.ru);
   c.r1 = T(s * pr.rv);
@@ -238,7 +303,7 @@ __device__ __forceinline__ CompactJ<T> linearise(const double* __restrict__ Rm, 
     c.J0 = c.J1 = c.J2 = c.v0 = c.v1 = c.v2 = c.F0 = c.F1 = T(0);
     return c;
   }
-  const double iz = 1.0 / pr.pc[2];
+  const double iz = pr.iz;
   const double fz = f * iz;
   c.J0 = T(s * fz);
   c.J1 = T(-s * fz * pr.pc[0] * iz);
@@ -254,7 +319,7 @@ __device__ __forceinline__ CompactJ<T> linearise(const double* __restrict__ Rm, 
 // Q = (Jp R) L^-T for one observation: two rows of 3 (forward substitution
 // with the point factor; L diagonal stored inverted).
 template <typename T>
-__device__ __forceinline__ void q_rows(T J0, T J1, T J2, const T (&Rt)[9], const T* __restrict__ L, T q[6]) {
+__device__ __forceinline__ void q_rows(T J0, T J1, T J2, const T* Rt, const T* __restrict__ L, T q[6]) {
   const T iL00 = L[0], L10 = L[1], iL11 = L[2], L20 = L[3], L21 = L[4], iL22 = L[5];
   T b[6];
 #pragma unroll
@@ -292,9 +357,11 @@ __device__ __forceinline__ void expand_A(T J0, T J1, T J2, T v0, T v1, T v2, T a
 
 // ---------------------------------------------------------------------------
 
-template <typename T, int R>
+template <typename T, int R, int NT>
 __device__ void solve_problem(const Params& P, unsigned char* smem) {
+  constexpr int NW = NT / 32;
   using F = Fixed<T>;
+  constexpr int JSTR = jstr<T>();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int rank = Clu<R>::rank();
   const int b = (int)(blockIdx.x / R);
@@ -312,7 +379,6 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   double* red = (double*)(smem + F::oRed);
   T* S = (T*)(smem + F::oS);
   T* job = (T*)(smem + F::oJob);
-  T* jsum = R > 1 ? (T*)(smem + F::oJsum) : job;
   T* invd = (T*)(smem + F::oInvd);
   unsigned short* tab = (unsigned short*)(smem + F::oTab);
   int* cam_ptr = (int*)(smem + F::oCamPtr);
@@ -322,10 +388,14 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   unsigned char* blk_a = smem + F::oBlkA;
   unsigned char* blk_b = smem + F::oBlkB;
   unsigned char* arena = smem + F::kBytes;
+  T* RcT = (T*)(smem + F::oRcT);
+  T* dcT = (T*)(smem + F::oDcT);
 
   __shared__ int s_flag, s_nf, s_nlp, s_npairs, s_job;
-  __shared__ int s_wtot[NW];
+  __shared__ int s_cf[2];   // panel pivot failure, double-buffered by panel parity
+  __shared__ int s_wtot[NW_MAX];
   int epoch = 0;
+  PROF_DECL
 
   const int64_t cb = D.cam_off[b], pb = D.pt_off[b], ob = D.obs_off[b];
   const int n = (int)(D.cam_off[b + 1] - cb);
@@ -362,31 +432,13 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     s_nf = nf;
     s_flag = (n > MAXN) ? 1 : 0;
   }
-  // validation of the whole problem (every CTA, so the verdict needs no exchange)
-  for (int k = tid; k < K; k += NT) {
-    const int pt = __ldg(&gobs[k].pt), c = __ldg(&gobs[k].cam);
-    if (pt < 0 || pt >= Pn || c < 0 || c >= n || (k > 0 && __ldg(&gobs[k - 1].pt) > pt)) s_flag = 1;
-  }
   __syncthreads();
   const int nf = s_nf, C = 6 * nf + (has_f ? 1 : 0), FI = C - 1, CA = C * (C + 3) / 2;
   const int nb = opt_pts ? nf * (nf + 1) / 2 : 0;
   double f = O.focal_in[b];
-  if (s_flag) {  // malformed problem: report and leave parameters untouched
-    if (lead) {
-      O.n_iters[b] = 0;
-      O.status[b] = -1;
-      O.focal_out[b] = f;
-    }
-    if (rank == 0) {
-      for (int i = tid; i < n * 9; i += NT) O.R_out[cb * 9 + i] = O.R_in[cb * 9 + i];
-      for (int i = tid; i < n * 3; i += NT) O.t_out[cb * 3 + i] = O.t_in[cb * 3 + i];
-    }
-    for (int i = rank * NT + tid; i < Pn * 3; i += R * NT)
-      O.points_out[pb * 3 + i] = O.points_in[pb * 3 + i];
-    return;
-  }
 
   // this CTA's observation slice [k0, k1): point-aligned cut near K r / R
+  // (binary search on the point-major order, verified below)
   auto lower_bound_pt = [&](int p) {
     int lo_i = 0, hi_i = K;
     while (lo_i < hi_i) {
@@ -400,7 +452,55 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     if (rank > 0) k0 = lower_bound_pt(__ldg(&gobs[(int)((int64_t)K * rank / R)].pt));
     if (rank < R - 1) k1 = lower_bound_pt(__ldg(&gobs[(int)((int64_t)K * (rank + 1) / R)].pt));
   }
-  const int nlo = k1 - k0;
+  const int nlo = k1 > k0 ? k1 - k0 : 0;
+  // stage the slice's 16-byte records in shared memory (one coalesced pass) and
+  // validate it there: index ranges, point-major order, slice boundary
+  float4* sobs = (float4*)arena;                                        // [nlo] u, v, cam, point slot
+  unsigned char* newpt = arena + al16(16 * (size_t)nlo);               // [nlo] scratch (setup only)
+  bool overflow = al16(16 * (size_t)nlo) + nlo > P.arena || nlo >= 65535;
+  if (tid == 0 && k1 < k0) s_flag = 1;
+  if (!overflow) {
+    for (int kl = tid; kl < nlo; kl += NT) {
+      const float4 rec = __ldg(reinterpret_cast<const float4*>(gobs) + k0 + kl);
+      const int c = __float_as_int(rec.z), pt = __float_as_int(rec.w);
+      if (pt < 0 || pt >= Pn || c < 0 || c >= n) s_flag = 1;
+      sobs[kl] = rec;
+    }
+    __syncthreads();
+    int cnt = 0;
+    for (int kl = tid; kl < nlo; kl += NT) {
+      const int pt = __float_as_int(sobs[kl].w);
+      const int prev = kl > 0 ? __float_as_int(sobs[kl - 1].w) : -1;
+      if (prev > pt) s_flag = 1;
+      newpt[kl] = prev != pt;
+      cnt += prev != pt;
+    }
+    if (tid == 0 && nlo > 0 && k1 < K && __ldg(&gobs[k1].pt) < __float_as_int(sobs[nlo - 1].w)) s_flag = 1;
+    double v[1] = {(double)cnt};
+    block_sum_d<NW, 1>(v, red);
+    if (tid == 0) s_nlp = (int)v[0];
+  }
+  __syncthreads();
+  {  // the cluster agrees on validity (malformed problems keep their parameters)
+    double v[1] = {s_flag ? 1.0 : 0.0};
+    __syncthreads();
+    cluster_sum<R, 1>(v, xch, epoch);
+    if (v[0] != 0.0) {
+      if (lead) {
+        O.n_iters[b] = 0;
+        O.status[b] = -1;
+        O.focal_out[b] = f;
+      }
+      if (rank == 0) {
+        for (int i = tid; i < n * 9; i += NT) O.R_out[cb * 9 + i] = O.R_in[cb * 9 + i];
+        for (int i = tid; i < n * 3; i += NT) O.t_out[cb * 3 + i] = O.t_in[cb * 3 + i];
+      }
+      for (int i = rank * NT + tid; i < Pn * 3; i += R * NT)
+        O.points_out[pb * 3 + i] = O.points_in[pb * 3 + i];
+      Clu<R>::sync();
+      return;
+    }
+  }
   // points [p_lo, p_hi) belong to this rank (unobserved points included: they
   // keep their value, dp = 0, as in the reference)
   const int p_lo = rank == 0 ? 0 : (k0 < K ? __ldg(&gobs[k0].pt) : Pn);
@@ -408,19 +508,8 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   if (O.points_in != O.points_out)
     for (int i = p_lo * 3 + tid; i < p_hi * 3; i += NT) O.points_out[pb * 3 + i] = O.points_in[pb * 3 + i];
 
-  // count observed points of the slice
-  {
-    int cnt = 0;
-    for (int kl = tid; kl < nlo; kl += NT)
-      cnt += (kl == 0 || __ldg(&gobs[k0 + kl].pt) != __ldg(&gobs[k0 + kl - 1].pt)) ? 1 : 0;
-    double v[1] = {(double)cnt};
-    block_sum_d<1>(v, red);
-    if (tid == 0) s_nlp = (int)v[0];
-    __syncthreads();
-  }
-  const int nlp = s_nlp;
-  // arena layout
-  float4* sobs = (float4*)arena;                                        // [nlo] u, v, cam, point slot
+  const int nlp = overflow ? 0 : s_nlp;
+  // arena layout (newpt scratch aliases the start of Xs; it is consumed first)
   double* Xs = (double*)(arena + al16(16 * (size_t)nlo));               // [nlp][3]
   T* jac = (T*)((unsigned char*)Xs + al16(24 * (size_t)nlp));           // [nlo][JSTR]
   T* pf = (T*)((unsigned char*)jac + al16(sizeof(T) * JSTR * (size_t)nlo));  // [nlp][PSTR]
@@ -429,20 +518,14 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   unsigned short* ptr = (unsigned short*)((unsigned char*)perm + al16(2 * (size_t)nlo));  // [nlp+1]
   unsigned* pairs = (unsigned*)((unsigned char*)ptr + al16(2 * (size_t)(nlp + 1)));
   const size_t fixed_need = (size_t)((unsigned char*)pairs - arena);
-  bool overflow = fixed_need > P.arena || nlo >= 65535;
+  overflow = overflow || fixed_need > P.arena;
 
   if (!overflow) {
-    // stage observations; slots by a block-wide scan of "first observation of a point"
+    // point slots: block-wide scan of "first observation of a point"
     int base = 0;
     for (int c0 = 0; c0 < nlo; c0 += NT) {
       const int kl = c0 + tid;
-      int flag = 0, pt = 0;
-      float4 rec = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (kl < nlo) {
-        rec = __ldg(reinterpret_cast<const float4*>(gobs) + k0 + kl);
-        pt = __float_as_int(rec.w);
-        flag = (kl == 0 || __ldg(&gobs[k0 + kl - 1].pt) != pt) ? 1 : 0;
-      }
+      const int flag = kl < nlo ? newpt[kl] : 0;
       const int inc = warp_incl_scan(flag, lane);
       if (lane == 31) s_wtot[wid] = inc;
       __syncthreads();
@@ -452,12 +535,11 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       for (int w = 0; w < NW; ++w) tot += s_wtot[w];
       if (kl < nlo) {
         const int sl = pre + inc - 1;
-        rec.w = __int_as_float(sl);
-        sobs[kl] = rec;
         if (flag) {
-          lpt[sl] = pt;
+          lpt[sl] = __float_as_int(sobs[kl].w);
           ptr[sl] = (unsigned short)kl;
         }
+        sobs[kl].w = __int_as_float(sl);
       }
       base += tot;
       __syncthreads();
@@ -560,7 +642,10 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
 
   // cost pass over the slice with camera set (Rs, ts), focal ft and points
   // X + frac * dp; cluster-summed (sum rho, sum e, sum e^2)
-  auto cost = [&](const double* Rs, const double* ts, double ft, double frac, bool use_dp, double out[3]) {
+  // (full: also sum e and sum e^2 for final_rms / mean_err, miniba.py:295-296)
+  auto cost = [&](auto full, const double* Rs, const double* ts, double ft, double frac, bool use_dp,
+                  double out[3]) {
+    constexpr bool FULL = decltype(full)::value;
     double acc[3] = {0.0, 0.0, 0.0};
     constexpr int U = 4;
     for (int c0 = tid; c0 < nlo; c0 += U * NT) {
@@ -582,15 +667,25 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         }
         double uu, vv;
         obs_uv(kl, o[u], uu, vv);
-        Proj pr = project_residual_fast(Rs + 9 * c, ts + 3 * c, Xp, ft, cx, cy, uu, vv);
-        const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
-        acc[0] += robust_rho(e, delta, loss);
-        acc[1] += e;
-        acc[2] += e * e;
+        const ProjZ pr = proj_z(Rs + 9 * c, ts + 3 * c, Xp, ft, cx, cy, uu, vv);
+        const double e2 = pr.ru * pr.ru + pr.rv * pr.rv;
+        acc[0] += rho_e2(e2, delta, loss);
+        if constexpr (FULL) {
+          const double e = sqrt(e2);
+          acc[1] += e;
+          acc[2] += e * e;
+        }
       }
     }
-    block_sum_d<3>(acc, red);
-    cluster_sum<R, 3>(acc, xch, epoch);
+    if constexpr (FULL) {
+      block_sum_d<NW, 3>(acc, red);
+      cluster_sum<R, 3>(acc, xch, epoch);
+    } else {
+      double a1[1] = {acc[0]};
+      block_sum_d<NW, 1>(a1, red);
+      cluster_sum<R, 1>(a1, xch, epoch);
+      acc[0] = a1[0];
+    }
     out[0] = acc[0];
     out[1] = acc[1];
     out[2] = acc[2];
@@ -601,16 +696,21 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   uint8_t* accepted = O.accepted + (size_t)b * max_it;
   uint8_t* evals = O.evals + (size_t)b * max_it;
 
+  for (int i = tid; i < n * 9; i += NT) RcT[i] = T(Rc[i]);
+  __syncthreads();
+  PROF_MARK(PH_SETUP)
   // initial cost (miniba.py:232-235)
   double st[3];
-  cost(Rc, tc, f, 0.0, false, st);
-  double cur = st[0], se = st[1], se2 = st[2];
+  cost(std::false_type(), Rc, tc, f, 0.0, false, st);
+  PROF_MARK(PH_COST0)
+  double cur = st[0];
   double lam = cfg.lambda_init;
   if (lead) costs[0] = cur;
   int it = 0, stop_reason = MBA_SOLVE_MAX_ITERS;
 
   for (; it < max_it;) {
     const T tlam = T(lam);
+    const T inv_f = T(1.0 / f);
     // ---------- point pass: compact Jacobians, V_p / g_p / Wf_p, point factor ----------
     T part[4] = {T(0), T(0), T(0), T(0)};  // U_ff, g_f, sum yf.yf, sum yf.z
     for (int sl = tid; sl < nlp; sl += NT) {
@@ -626,19 +726,18 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         const CompactJ<T> cj = linearise<T>(Rc + 9 * c, tc + 3 * c, Xp, f, cx, cy, uu, vv, delta, loss);
         T* jk = jac + (size_t)kl * JSTR;
         jk[0] = cj.J0; jk[1] = cj.J1; jk[2] = cj.J2;
-        jk[3] = cj.v0; jk[4] = cj.v1; jk[5] = cj.v2;
-        jk[6] = cj.F0; jk[7] = cj.F1; jk[8] = cj.r0; jk[9] = cj.r1;
+        if constexpr (JSTR == 5) { jk[3] = cj.r0; jk[4] = cj.r1; }
         if (has_f) {
           part[0] += cj.F0 * cj.F0 + cj.F1 * cj.F1;
           part[1] += cj.F0 * cj.r0 + cj.F1 * cj.r1;
         }
         if (opt_pts) {
-          const double* Rk = Rc + 9 * c;
+          const T* Rk = RcT + 9 * c;
           T B0[3], B1[3];
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
-            B0[q] = cj.J0 * T(Rk[q]) + cj.J1 * T(Rk[6 + q]);
-            B1[q] = cj.J0 * T(Rk[3 + q]) + cj.J2 * T(Rk[6 + q]);
+            B0[q] = cj.J0 * Rk[q] + cj.J1 * Rk[6 + q];
+            B1[q] = cj.J0 * Rk[3 + q] + cj.J2 * Rk[6 + q];
           }
           V[0] += B0[0] * B0[0] + B1[0] * B1[0];
           V[1] += B0[1] * B0[0] + B1[1] * B1[0];
@@ -691,6 +790,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       }
     }
 
+    PROF_MARK(PH_POINT)
     // ---------- camera jobs + pair jobs (warps pull jobs from a queue) ----------
     for (;;) {
       int jb = 0;
@@ -701,16 +801,37 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         const int s = jb, c = cslot[s];
         T Rt9[9];
 #pragma unroll
-        for (int i = 0; i < 9; ++i) Rt9[i] = T(Rc[9 * c + i]);
+        for (int i = 0; i < 9; ++i) Rt9[i] = RcT[9 * c + i];
+        const T t0 = T(tc[3 * c]), t1 = T(tc[3 * c + 1]), t2 = T(tc[3 * c + 2]);
         T acc[UST];
 #pragma unroll
         for (int i = 0; i < UST; ++i) acc[i] = T(0);
         for (int q = cam_ptr[c] + lane; q < cam_ptr[c + 1]; q += 32) {
           const int kl = perm[q];
+          const float4 ob = sobs[kl];
+          const int sl = __float_as_int(ob.w);
           const T* jk = jac + (size_t)kl * JSTR;
-          const T J0 = jk[0], J1 = jk[1], J2 = jk[2], F0 = jk[6], F1 = jk[7], r0 = jk[8], r1 = jk[9];
+          const T J0 = jk[0], J1 = jk[1], J2 = jk[2];
+          // v = R X; F = sqrt(w) (x, y)/z = (J0/f)(x, y); r (fp64) = J0 x + (J0 z/f)(c - u)
+          const T X0 = T(Xs[3 * sl]), X1 = T(Xs[3 * sl + 1]), X2 = T(Xs[3 * sl + 2]);
+          const T v0 = Rt9[0] * X0 + Rt9[1] * X1 + Rt9[2] * X2;
+          const T v1 = Rt9[3] * X0 + Rt9[4] * X1 + Rt9[5] * X2;
+          const T v2 = Rt9[6] * X0 + Rt9[7] * X1 + Rt9[8] * X2;
+          const T sz = J0 * inv_f;   // sqrt(w) / z
+          const T F0 = (v0 + t0) * sz, F1 = (v1 + t1) * sz;
+          T r0, r1;
+          if constexpr (JSTR == 5) {
+            r0 = jk[3];
+            r1 = jk[4];
+          } else {
+            double uu, vv;
+            obs_uv(kl, ob, uu, vv);
+            const T sw = sz * (v2 + t2);   // sqrt(w)
+            r0 = J0 * (v0 + t0) + sw * T(cx - uu);
+            r1 = J0 * (v1 + t1) + sw * T(cy - vv);
+          }
           T a[12];
-          expand_A(J0, J1, J2, jk[3], jk[4], jk[5], a);
+          expand_A(J0, J1, J2, v0, v1, v2, a);
           int idx = 0;
 #pragma unroll
           for (int r = 0; r < 6; ++r) {
@@ -720,7 +841,6 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
             acc[27 + r] += a[r] * r0 + a[6 + r] * r1;
           }
           if (opt_pts) {
-            const int sl = __float_as_int(sobs[kl].w);
             const T* pw = pf + (size_t)sl * PSTR;
             T qv[6];
             q_rows(J0, J1, J2, Rt9, pw, qv);
@@ -742,8 +862,8 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         T Ra[9], Rb[9];
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
-          Ra[i] = T(Rc[9 * ca + i]);
-          Rb[i] = T(Rc[9 * cbb + i]);
+          Ra[i] = RcT[9 * ca + i];
+          Rb[i] = RcT[9 * cbb + i];
         }
         T acc[36];
 #pragma unroll
@@ -752,11 +872,20 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         for (int q = blk_off[blk] + lane; q < q1; q += 32) {
           const unsigned pr = pairs[q];
           const int i = (int)(pr >> 16), j = (int)(pr & 0xffffu);
-          const T* pw = pf + (size_t)__float_as_int(sobs[i].w) * PSTR;
+          const int sl = __float_as_int(sobs[i].w);
+          const T* pw = pf + (size_t)sl * PSTR;
           const T* ji = jac + (size_t)i * JSTR;
           const T* jj = jac + (size_t)j * JSTR;
-          const T Ji0 = ji[0], Ji1 = ji[1], Ji2 = ji[2], vi0 = ji[3], vi1 = ji[4], vi2 = ji[5];
-          const T Jj0 = jj[0], Jj1 = jj[1], Jj2 = jj[2], vj0 = jj[3], vj1 = jj[4], vj2 = jj[5];
+          const T Ji0 = ji[0], Ji1 = ji[1], Ji2 = ji[2];
+          const T Jj0 = jj[0], Jj1 = jj[1], Jj2 = jj[2];
+          // v_i = R_a X_p, v_j = R_b X_p (same point)
+          const T X0 = T(Xs[3 * sl]), X1 = T(Xs[3 * sl + 1]), X2 = T(Xs[3 * sl + 2]);
+          const T vi0 = Ra[0] * X0 + Ra[1] * X1 + Ra[2] * X2;
+          const T vi1 = Ra[3] * X0 + Ra[4] * X1 + Ra[5] * X2;
+          const T vi2 = Ra[6] * X0 + Ra[7] * X1 + Ra[8] * X2;
+          const T vj0 = Rb[0] * X0 + Rb[1] * X1 + Rb[2] * X2;
+          const T vj1 = Rb[3] * X0 + Rb[4] * X1 + Rb[5] * X2;
+          const T vj2 = Rb[6] * X0 + Rb[7] * X1 + Rb[8] * X2;
           T qi[6], qj[6];
           q_rows(Ji0, Ji1, Ji2, Ra, pw, qi);
           q_rows(Jj0, Jj1, Jj2, Rb, pw, qj);
@@ -800,19 +929,17 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       }
     }
     Clu<R>::sync();  // every CTA's job outputs are complete and visible
-    if constexpr (R > 1) {
-      const T* rj[R];
+    // cluster totals of the job outputs, summed in rank order on access
+    const T* rjob[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) rj[r] = Clu<R>::remote(job, r);
-      for (int i = tid; i < JOB_OUT; i += NT) {
-        T s_ = T(0);
+    for (int r = 0; r < R; ++r) rjob[r] = Clu<R>::remote(job, r);
+    auto jsum_at = [&](int i) {
+      T s_ = rjob[0][i];
 #pragma unroll
-        for (int r = 0; r < R; ++r) s_ += rj[r][i];
-        jsum[i] = s_;
-      }
-      __syncthreads();
-    }
-
+      for (int r = 1; r < R; ++r) s_ += rjob[r][i];
+      return s_;
+    };
+    PROF_MARK(PH_JOBS)
     // ---------- assemble the damped augmented reduced system (miniba.py:188-213) ----------
     for (int e = tid; e < CA; e += NT) {
       const unsigned ij = tab[e];
@@ -820,19 +947,19 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       T val;
       if (i == C) {                       // rhs row
         if (j == FI && has_f) {
-          val = -jsum[JOB_PART + 1] + (opt_pts ? jsum[JOB_PART + 3] : T(0));
+          val = -jsum_at(JOB_PART + 1) + (opt_pts ? jsum_at(JOB_PART + 3) : T(0));
         } else {
-          const T* u = jsum + (j / 6) * UST;
-          val = -u[27 + j % 6] + (opt_pts ? u[39 + j % 6] : T(0));
+          const int u = (j / 6) * UST;
+          val = -jsum_at(u + 27 + j % 6) + (opt_pts ? jsum_at(u + 39 + j % 6) : T(0));
         }
       } else if (has_f && i == FI) {      // focal row
         if (j == FI) {
-          const T uff = jsum[JOB_PART + 0];
+          const T uff = jsum_at(JOB_PART + 0);
           val = uff + tlam * (uff > T(kDiagFloor) ? uff : T(kDiagFloor)) -
-                (opt_pts ? jsum[JOB_PART + 2] : T(0));
+                (opt_pts ? jsum_at(JOB_PART + 2) : T(0));
         } else {
-          const T* u = jsum + (j / 6) * UST;
-          val = u[21 + j % 6] - (opt_pts ? u[33 + j % 6] : T(0));
+          const int u = (j / 6) * UST;
+          val = jsum_at(u + 21 + j % 6) - (opt_pts ? jsum_at(u + 33 + j % 6) : T(0));
         }
       } else {                            // camera-camera: i >= j
         const int sb = i / 6, sa = j / 6, ri = i % 6, rj = j % 6;
@@ -840,16 +967,16 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         val = T(0);
         if (sa == sb) {
           const int r = ri, cc = rj;  // r >= cc
-          T ud = jsum[sa * UST + r * (r + 1) / 2 + cc];
+          T ud = jsum_at(sa * UST + r * (r + 1) / 2 + cc);
           if (r == cc) ud += tlam * (ud > T(kDiagFloor) ? ud : T(kDiagFloor));
           val = ud;
           if (opt_pts) {
             const int q = sa * nf - sa * (sa - 1) / 2;   // block (sa, sa)
-            schur = jsum[JOB_PAIR0 + q * 36 + r * 6 + cc];
+            schur = jsum_at(JOB_PAIR0 + q * 36 + r * 6 + cc);
           }
         } else if (opt_pts) {
           const int q = sa * nf - sa * (sa - 1) / 2 + (sb - sa);   // block (sa, sb)
-          schur = jsum[JOB_PAIR0 + q * 36 + rj * 6 + ri];
+          schur = jsum_at(JOB_PAIR0 + q * 36 + rj * 6 + ri);
         }
         val -= schur;
       }
@@ -857,24 +984,44 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     }
     __syncthreads();
 
-    // ---------- LDL^T of the augmented system, one barrier per column ----------
+    PROF_MARK(PH_ASM)
+    // ---------- LDL^T of the augmented system ----------
+    // Column-by-column right-looking elimination of the packed augmented
+    // system, one barrier per column; each thread updates up to 4 entries per
+    // column with all loads issued before the arithmetic (no dependent load
+    // chain per entry). S[k][k] keeps d_k, S[i][k] keeps L_ik d_k; the rhs
+    // row C receives the forward substitution y = L^-1 b.
     bool chol_fail = false;
     for (int k = 0; k < C; ++k) {
       const T* colk = S + acol(k, C) - k;  // colk[i] = S[i][k], i in [k, C]
+      const int e0 = acol(k + 1, C);
       const T d = colk[k];
-      if (!(d > T(0)) || !isfinite((double)d)) {
-        chol_fail = true;  // uniform: every thread reads the same pivot
+      if (!(d > T(0)) || !isfinite(d)) {
+        chol_fail = true;  // every thread reads the same pivot: uniform exit
         break;
       }
-      const T inv = T(1) / d;
-      if (tid == 0) invd[k] = inv;
-      for (int e = acol(k + 1, C) + tid; e < CA; e += NT) {
-        const unsigned ij = tab[e];
-        S[e] -= colk[ij >> 8] * colk[ij & 255u] * inv;
+      for (int eb = e0 + tid; eb < CA; eb += 4 * NT) {
+        unsigned ij[4];
+        T ci[4], cj[4], sv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ij[u] = eb + u * NT < CA ? tab[eb + u * NT] : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ci[u] = colk[ij[u] >> 8];
+          cj[u] = colk[ij[u] & 255u];
+          sv[u] = eb + u * NT < CA ? S[eb + u * NT] : T(0);
+        }
+        const T inv = T(1) / d;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (eb + u * NT < CA) S[eb + u * NT] = sv[u] - ci[u] * cj[u] * inv;
       }
+      if (tid == 0) invd[k] = T(1) / d;
       __syncthreads();
     }
+    PROF_MARK(PH_CHA)
     if (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull)) chol_fail = true;
+    PROF_MARK(PH_CHOL)
 
     if (!chol_fail) {
       // column-oriented back substitution D L^T x = y in warp 0 (no reductions):
@@ -891,33 +1038,36 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
           if (lane < k) u0 -= S[acol(lane, C) + k - lane] * xk;
           if (lane + 32 < k) u1 -= S[acol(lane + 32, C) + k - lane - 32] * xk;
         }
-        if (lane < C) dc[lane] = (double)u0;
-        if (lane + 32 < C) dc[lane + 32] = (double)u1;
+        if (lane < C) { dc[lane] = (double)u0; dcT[lane] = u0; }
+        if (lane + 32 < C) { dc[lane + 32] = (double)u1; dcT[lane + 32] = u1; }
       }
       __syncthreads();
       // point back substitution (miniba.py:216-217): dp = -L^-T (z + yf df + sum Y_i^T dc_a)
       if (opt_pts) {
-        const T df = has_f ? T(dc[FI]) : T(0);
+        const T df = has_f ? dcT[FI] : T(0);
         for (int sl = tid; sl < nlp; sl += NT) {
           T* pw = pf + (size_t)sl * PSTR;
+          const T X0 = T(Xs[3 * sl]), X1 = T(Xs[3 * sl + 1]), X2 = T(Xs[3 * sl + 2]);
           T u0 = pw[6] + pw[9] * df, u1 = pw[7] + pw[10] * df, u2 = pw[8] + pw[11] * df;
           for (int kl = ptr[sl]; kl < ptr[sl + 1]; ++kl) {
             const int c = __float_as_int(sobs[kl].z);
             const int s = slot[c];
             if (s < 0) continue;
             const T* jk = jac + (size_t)kl * JSTR;
-            const T J0 = jk[0], J1 = jk[1], J2 = jk[2], v0 = jk[3], v1 = jk[4], v2 = jk[5];
-            const T w0 = T(dc[6 * s]), w1 = T(dc[6 * s + 1]), w2 = T(dc[6 * s + 2]);
+            const T J0 = jk[0], J1 = jk[1], J2 = jk[2];
+            const T* Rk = RcT + 9 * c;
+            const T v0 = Rk[0] * X0 + Rk[1] * X1 + Rk[2] * X2;
+            const T v1 = Rk[3] * X0 + Rk[4] * X1 + Rk[5] * X2;
+            const T v2 = Rk[6] * X0 + Rk[7] * X1 + Rk[8] * X2;
+            const T* dca = dcT + 6 * s;
+            const T w0 = dca[0], w1 = dca[1], w2 = dca[2];
             // G dc = -(v x w) + dt ; A dc = Jp (G dc)
-            const T g0 = -(v1 * w2 - v2 * w1) + T(dc[6 * s + 3]);
-            const T g1 = -(v2 * w0 - v0 * w2) + T(dc[6 * s + 4]);
-            const T g2 = -(v0 * w1 - v1 * w0) + T(dc[6 * s + 5]);
+            const T g0 = -(v1 * w2 - v2 * w1) + dca[3];
+            const T g1 = -(v2 * w0 - v0 * w2) + dca[4];
+            const T g2 = -(v0 * w1 - v1 * w0) + dca[5];
             const T ad0 = J0 * g0 + J1 * g2, ad1 = J0 * g1 + J2 * g2;
-            T Rt9[9];
-#pragma unroll
-            for (int i = 0; i < 9; ++i) Rt9[i] = T(Rc[9 * c + i]);
             T qv[6];
-            q_rows(J0, J1, J2, Rt9, pw, qv);
+            q_rows(J0, J1, J2, RcT + 9 * c, pw, qv);
             u0 += qv[0] * ad0 + qv[3] * ad1;
             u1 += qv[1] * ad0 + qv[4] * ad1;
             u2 += qv[2] * ad0 + qv[5] * ad1;
@@ -933,6 +1083,8 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       }
     }
 
+    __syncthreads();
+    PROF_MARK(PH_SOLVE)
     // ---------- trials, accept / reject, lambda (miniba.py:244-293) ----------
     if (lead) lambdas[it] = lam;
     int tries = 0, took = -1;
@@ -959,7 +1111,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       for (int bt = 0; bt < kBacktrackTries; ++bt) {
         const double frac = ldexp(1.0, -bt);
         ft = has_f ? f + frac * dc[FI] : f;
-        cost(Rt + (size_t)bt * n * 9, tt + (size_t)bt * n * 3, ft, frac, opt_pts, tc_);
+        cost(std::false_type(), Rt + (size_t)bt * n * 9, tt + (size_t)bt * n * 3, ft, frac, opt_pts, tc_);
         ++tries;
         if (tc_[0] < cur && isfinite(tc_[0])) {
           took = bt;
@@ -969,12 +1121,14 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     } else {
       Clu<R>::sync();  // job buffers are rewritten next iteration: peers must be done reading
     }
+    PROF_MARK(PH_TRIAL)
     if (lead) evals[it] = (uint8_t)tries;
     bool stop = false;
     if (took >= 0) {
       const double frac = ldexp(1.0, -took);
       for (int i = tid; i < n * 9; i += NT) Rc[i] = Rt[(size_t)took * n * 9 + i];
       for (int i = tid; i < n * 3; i += NT) tc[i] = tt[(size_t)took * n * 3 + i];
+      for (int i = tid; i < n * 9; i += NT) RcT[i] = T(Rt[(size_t)took * n * 9 + i]);
       if (opt_pts)
         for (int i = tid; i < nlp * 3; i += NT) {
           const T* dp = pf + (size_t)(i / 3) * PSTR + 12;
@@ -984,8 +1138,6 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       lam = took == 0 ? fmax(lam / nu, 1e-15) : fmin(lam * nu, kLambdaMax);
       const double improve = cur - tc_[0];
       cur = tc_[0];
-      se = tc_[1];
-      se2 = tc_[2];
       if (lead) accepted[it] = 1;
       if (improve <= 1e-15 * fmax(cur, 1.0)) {
         stop = true;
@@ -1002,10 +1154,13 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     if (lead) costs[it + 1] = cur;
     ++it;
     __syncthreads();
+    PROF_MARK(PH_COMMIT)
     if (stop) break;
   }
 
   // ---------------- outputs ----------------
+  cost(std::true_type(), Rc, tc, f, 0.0, false, st);   // sum e, sum e^2 of the final state
+  const double se = st[1], se2 = st[2];
   for (int i = tid; i < nlp * 3; i += NT) O.points_out[(pb + lpt[i / 3]) * 3 + i % 3] = Xs[i];
   if (rank == 0) {
     for (int i = tid; i < n * 9; i += NT) O.R_out[cb * 9 + i] = Rc[i];
@@ -1020,13 +1175,14 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     O.final_stats[4 * b + 2] = se2;
     O.final_stats[4 * b + 3] = (double)K;
   }
+  PROF_FLUSH
   Clu<R>::sync();  // no CTA leaves while a peer may still read its shared memory
 }
 
-template <typename T, int R, int MINB>
+template <typename T, int R, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) solve_v4_kernel(Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
-  solve_problem<T, R>(P, smem);
+  solve_problem<T, R, NT>(P, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1041,36 +1197,61 @@ static size_t need_bytes(const MbaBatchDesc* d, int R) {
   return Fixed<T>::kBytes + obs * obs_bytes<T>() + pts * pt_bytes<T>() + 4 * prs + 8 * 16;
 }
 
-template <typename T>
-static int plan_t(const MbaBatchDesc* d) {
-  if (const char* e = getenv("MBA_V4_R")) {
-    const int r = atoi(e);
-    if (r == 1 || r == 2 || r == 4 || r == 8 || r == 16) return need_bytes<T>(d, r) <= kSmemLimit ? r : 0;
-  }
-  for (int R : {1, 2, 4, 8, 16})
-    if (need_bytes<T>(d, R) <= kSmemLimit) return R;
-  return 0;
+// dynamic shared memory a CTA can use at `per_sm` CTAs per SM (228 KB per SM,
+// 1 KB reserved per CTA, static shared memory of the kernel excluded)
+static size_t smem_per_cta(int per_sm, size_t static_bytes) {
+  size_t per = (228 * 1024) / (size_t)per_sm - 1024 - static_bytes;
+  return per < kSmemLimit - static_bytes ? per : kSmemLimit - static_bytes;
 }
 
-int plan_cluster(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
-  if (d->max_cams > MAXN || d->max_cams < 1 || d->max_obs >= 65535 * 16) return 0;
+struct Plan {
+  int R, nt, per_sm;
+};
+
+// Smallest cluster that fits (every CTA of a cluster repeats the serial
+// phases -- LDL^T, substitutions, step control -- so splitting a problem costs
+// more than it gains; measured on config 4: R=1 247k problems/s (mixed) vs R=2
+// 149k); at equal R prefer two co-resident problems per SM. Overrides:
+// MBA_V4_R, MBA_V4_NT, MBA_V4_PERSM.
+template <typename T>
+static Plan plan_t(const MbaBatchDesc* d) {
+  const int eR = getenv("MBA_V4_R") ? atoi(getenv("MBA_V4_R")) : 0;
+  const int eP = getenv("MBA_V4_PERSM") ? atoi(getenv("MBA_V4_PERSM")) : 0;
+  const int eN = getenv("MBA_V4_NT") ? atoi(getenv("MBA_V4_NT")) : 0;
+  const size_t st = 256;   // static shared memory bound
+  for (int R : {1, 2, 4, 8, 16}) {
+    if (eR && R != eR) continue;
+    for (int per_sm : {2, 1}) {
+      if (eP && per_sm != eP) continue;
+      if (per_sm == 2 && R > 4) continue;
+      if (need_bytes<T>(d, R) <= smem_per_cta(per_sm, st)) {
+        int nt = per_sm == 2 ? (sizeof(T) == 8 ? 128 : 256) : 256;
+        if (eN == 128 || eN == 256) nt = eN;
+        if (per_sm == 2 && sizeof(T) == 8) nt = 128;   // 255 registers need 128 threads at 2 CTAs/SM
+        return Plan{R, nt, per_sm};
+      }
+    }
+  }
+  return Plan{0, 0, 0};
+}
+
+static Plan plan(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
+  if (d->max_cams > MAXN || d->max_cams < 1 || d->max_obs >= 65535 * 16) return Plan{0, 0, 0};
   return cfg->precision == MBA_LIN_F64 ? plan_t<double>(d) : plan_t<float>(d);
 }
 
-template <typename T, int R, int MINB>
+int plan_cluster(const MbaBatchDesc* d, const MbaLmConfig* cfg) { return plan(d, cfg).R; }
+
+template <typename T, int R, int NT, int MINB>
 static int launch_t(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st) {
-  auto kern = solve_v4_kernel<T, R, MINB>;
+  auto kern = solve_v4_kernel<T, R, NT, MINB>;
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return MBA_ERR_CUDA;
-  size_t smem = need_bytes<T>(d, R);
-  const size_t cap = kSmemLimit - fa.sharedSizeBytes;
-  if (smem > cap) return MBA_ERR_TOO_LARGE;
+  const size_t need = need_bytes<T>(d, R);
   // take all the shared memory a CTA gets at this occupancy (slack for
-  // unbalanced slices before the overflow fallback triggers); 228 KB per SM,
-  // 1 KB reserved per CTA
-  size_t per = (228 * 1024) / (size_t)MINB - 1024 - fa.sharedSizeBytes;
-  if (per > cap) per = cap;
-  if (smem < per) smem = per;
+  // unbalanced slices before the overflow fallback triggers)
+  const size_t smem = smem_per_cta(MINB, fa.sharedSizeBytes);
+  if (need > smem) return MBA_ERR_TOO_LARGE;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     if (getenv("MBA_DEBUG")) fprintf(stderr, "mba v4 smem attribute %zu rejected\n", smem);
     return MBA_ERR_CUDA;
@@ -1095,29 +1276,45 @@ static int launch_t(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutp
   lc.numAttrs = 1;
   const cudaError_t err = cudaLaunchKernelEx(&lc, kern, P);
   if (err != cudaSuccess && getenv("MBA_DEBUG"))
-    fprintf(stderr, "mba v4 launch (R=%d, smem=%zu): %s\n", R, smem, cudaGetErrorString(err));
+    fprintf(stderr, "mba v4 launch (R=%d, NT=%d, smem=%zu): %s\n", R, NT, smem, cudaGetErrorString(err));
   return err == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
 }
 
 template <typename T>
 static int launch_prec(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st,
-                       int R) {
-  constexpr int MB = sizeof(T) == 4 ? 2 : 1;
-  switch (R) {
-    case 1: return need_bytes<T>(d, 1) * 2 + 2048 <= kSmemLimit ? launch_t<T, 1, 2>(d, cfg, o, st)
-                                                                : launch_t<T, 1, 1>(d, cfg, o, st);
-    case 2: return need_bytes<T>(d, 2) * 2 + 2048 <= kSmemLimit ? launch_t<T, 2, 2>(d, cfg, o, st)
-                                                                : launch_t<T, 2, 1>(d, cfg, o, st);
-    case 4: return launch_t<T, 4, MB>(d, cfg, o, st);
-    case 8: return launch_t<T, 8, 1>(d, cfg, o, st);
-    case 16: return launch_t<T, 16, 1>(d, cfg, o, st);
+                       const Plan& p) {
+  if (getenv("MBA_DEBUG")) fprintf(stderr, "mba v4 plan: R=%d NT=%d per_sm=%d\n", p.R, p.nt, p.per_sm);
+  if (p.per_sm == 2) {
+    if (p.nt == 128) {
+      switch (p.R) {
+        case 1: return launch_t<T, 1, 128, 2>(d, cfg, o, st);
+        case 2: return launch_t<T, 2, 128, 2>(d, cfg, o, st);
+        case 4: return launch_t<T, 4, 128, 2>(d, cfg, o, st);
+      }
+    } else if constexpr (sizeof(T) == 4) {
+      switch (p.R) {
+        case 1: return launch_t<T, 1, 256, 2>(d, cfg, o, st);
+        case 2: return launch_t<T, 2, 256, 2>(d, cfg, o, st);
+        case 4: return launch_t<T, 4, 256, 2>(d, cfg, o, st);
+      }
+    }
+    return MBA_ERR_TOO_LARGE;
+  }
+  switch (p.R) {
+    case 1: return launch_t<T, 1, 256, 1>(d, cfg, o, st);
+    case 2: return launch_t<T, 2, 256, 1>(d, cfg, o, st);
+    case 4: return launch_t<T, 4, 256, 1>(d, cfg, o, st);
+    case 8: return launch_t<T, 8, 256, 1>(d, cfg, o, st);
+    case 16: return launch_t<T, 16, 256, 1>(d, cfg, o, st);
     default: return MBA_ERR_TOO_LARGE;
   }
 }
 
 int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st, int R) {
-  if (cfg->precision == MBA_LIN_F64) return launch_prec<double>(d, cfg, o, st, R);
-  return launch_prec<float>(d, cfg, o, st, R);
+  Plan p = plan(d, cfg);
+  if (p.R != R || R == 0) return MBA_ERR_TOO_LARGE;
+  if (cfg->precision == MBA_LIN_F64) return launch_prec<double>(d, cfg, o, st, p);
+  return launch_prec<float>(d, cfg, o, st, p);
 }
 
 }  // namespace v4

@@ -25,5 +25,9 @@ int plan_cluster(const MbaBatchDesc* d, const MbaLmConfig* cfg);
 int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st,
            int cluster);
 
+#ifdef MBA_PHASE_PROF
+void set_prof(unsigned long long* p);
+#endif
+
 }  // namespace v4
 }  // namespace mba

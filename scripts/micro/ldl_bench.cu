@@ -1,0 +1,205 @@
+// Microbenchmark: LDL^T of the packed augmented reduced system (C = 43) in
+// shared memory, one CTA of 256 threads, clock64 per factorisation.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 ldl_bench.cu -o ldl_bench
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include <vector>
+
+__host__ __device__ __forceinline__ int acol(int j, int C) { return j * (C + 1) - (j * (j - 1)) / 2; }
+
+constexpr int NT = 256;
+constexpr int MAXCA = 49 * 52 / 2;
+
+template <typename T, int V>
+__global__ void bench(const T* __restrict__ Ain, int C, int reps, long long* cyc, T* out) {
+  __shared__ T S[MAXCA], S0[MAXCA], invd[64];
+  __shared__ unsigned short tab[MAXCA];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int CA = C * (C + 3) / 2;
+  for (int i = tid; i < CA; i += NT) S0[i] = Ain[i];
+  for (int j = tid; j < C; j += NT) {
+    const int a0 = acol(j, C);
+    for (int i = j; i <= C; ++i) tab[a0 + i - j] = (unsigned short)((i << 8) | j);
+  }
+  __syncthreads();
+  long long tot = 0;
+  for (int r = 0; r < reps; ++r) {
+    for (int i = tid; i < CA; i += NT) S[i] = S0[i];
+    __syncthreads();
+    long long t0 = clock64();
+    if constexpr (V == 0) {   // all threads, 1 barrier per column, unrolled x4
+      for (int k = 0; k < C; ++k) {
+        const T* colk = S + acol(k, C) - k;
+        const int e0 = acol(k + 1, C);
+        const T d = colk[k];
+        for (int eb = e0 + tid; eb < CA; eb += 4 * NT) {
+          unsigned ij[4]; T ci[4], cj[4], sv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) ij[u] = eb + u * NT < CA ? tab[eb + u * NT] : 0u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) { ci[u] = colk[ij[u] >> 8]; cj[u] = colk[ij[u] & 255u]; sv[u] = eb + u * NT < CA ? S[eb + u * NT] : T(0); }
+          const T inv = T(1) / d;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) if (eb + u * NT < CA) S[eb + u * NT] = sv[u] - ci[u] * cj[u] * inv;
+        }
+        if (tid == 0) invd[k] = T(1) / d;
+        __syncthreads();
+      }
+    } else if constexpr (V == 1) {  // one warp, syncwarp per column, unrolled x4
+      if (wid == 0) {
+        for (int k = 0; k < C; ++k) {
+          const T* colk = S + acol(k, C) - k;
+          const int e0 = acol(k + 1, C);
+          const T d = colk[k];
+          const T inv = T(1) / d;
+          for (int eb = e0 + lane; eb < CA; eb += 4 * 32) {
+            unsigned ij[4]; T ci[4], cj[4], sv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ij[u] = eb + u * 32 < CA ? tab[eb + u * 32] : 0u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { ci[u] = colk[ij[u] >> 8]; cj[u] = colk[ij[u] & 255u]; sv[u] = eb + u * 32 < CA ? S[eb + u * 32] : T(0); }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) if (eb + u * 32 < CA) S[eb + u * 32] = sv[u] - ci[u] * cj[u] * inv;
+          }
+          if (lane == 0) invd[k] = inv;
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+    } else if constexpr (V == 2) {  // one warp, lane = row (rows l, l+32), smem, loop over columns j
+      if (wid == 0) {
+        const int i0 = lane, i1 = lane + 32;
+        for (int k = 0; k < C; ++k) {
+          const T* colk = S + acol(k, C) - k;
+          const T d = colk[k];
+          const T inv = T(1) / d;
+          const T l0 = (i0 > k && i0 <= C) ? colk[i0] * inv : T(0);
+          const T l1 = (i1 > k && i1 <= C) ? colk[i1] * inv : T(0);
+          const int jmax = (i1 <= C ? i1 : (i0 <= C ? i0 : -1));
+          // row i updates entries j in (k, min(i, C-1)]
+#pragma unroll 4
+          for (int j = k + 1; j < C; ++j) {
+            const T cjk = colk[j];
+            T* colj = S + acol(j, C) - j;
+            if (i0 >= j && i0 <= C) colj[i0] -= l0 * cjk;
+            if (i1 >= j && i1 <= C) colj[i1] -= l1 * cjk;
+          }
+          if (lane == 0) invd[k] = inv;
+          __syncwarp();
+          (void)jmax;
+        }
+      }
+      __syncthreads();
+    } else if constexpr (V == 3) {  // all threads, 2 columns per barrier (rank-2 step)
+      int k = 0;
+      for (; k + 1 < C; k += 2) {
+        const T* colk = S + acol(k, C) - k;
+        T* colk1 = S + acol(k + 1, C) - (k + 1);
+        const T d0 = colk[k];
+        const T i0 = T(1) / d0;
+        const T l10 = colk[k + 1] * i0;                  // L_{k+1,k}
+        const T d1 = colk1[k + 1] - l10 * colk[k + 1];
+        const T i1 = T(1) / d1;
+        const int e0 = acol(k + 2, C);
+        for (int eb = e0 + tid; eb < CA; eb += 2 * NT) {
+          unsigned ij[2]; T a[2], b[2], c[2], dd[2], sv[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) ij[u] = eb + u * NT < CA ? tab[eb + u * NT] : 0u;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int i = ij[u] >> 8, j = ij[u] & 255u;
+            a[u] = colk[i]; b[u] = colk[j]; c[u] = colk1[i]; dd[u] = colk1[j];
+            sv[u] = eb + u * NT < CA ? S[eb + u * NT] : T(0);
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const T ci1 = c[u] - a[u] * l10, cj1 = dd[u] - b[u] * l10;   // column k+1 after step k
+            if (eb + u * NT < CA) S[eb + u * NT] = sv[u] - a[u] * b[u] * i0 - ci1 * cj1 * i1;
+          }
+        }
+        __syncthreads();
+        // finalise column k+1 (rows k+1..C) -- disjoint from the trailing region
+        for (int i = k + 1 + tid; i <= C; i += NT) colk1[i] = (i == k + 1) ? d1 : colk1[i] - colk[i] * l10;
+        if (tid == 0) { invd[k] = i0; invd[k + 1] = i1; }
+        __syncthreads();
+      }
+      for (; k < C; ++k) {
+        const T* colk = S + acol(k, C) - k;
+        const T d = colk[k];
+        for (int e = acol(k + 1, C) + tid; e < CA; e += NT) { const unsigned ij = tab[e]; S[e] -= colk[ij >> 8] * colk[ij & 255u] / d; }
+        if (tid == 0) invd[k] = T(1) / d;
+        __syncthreads();
+      }
+    } else if constexpr (V == 4) {  // barrier only
+      for (int k = 0; k < C; ++k) __syncthreads();
+    } else if constexpr (V == 5) {  // LDS -> STS chain + barrier
+      for (int k = 0; k < C; ++k) {
+        const T d = S[acol(k, C)];
+        if (tid < CA) S[(tid + k) % CA] = d + T(1);
+        __syncthreads();
+      }
+    } else if constexpr (V == 6) {  // register-owned entries (5 per thread), publish column k+1
+      constexpr int E = 5;
+      T v[E]; int ii[E], jj[E], ee[E];
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        ee[u] = tid + u * NT;
+        const unsigned ij = ee[u] < CA ? tab[ee[u]] : 0u;
+        ii[u] = ij >> 8; jj[u] = ij & 255u;
+        v[u] = ee[u] < CA ? S[ee[u]] : T(0);
+      }
+      for (int k = 0; k < C; ++k) {
+        const T* colk = S + acol(k, C) - k;
+        const T d = colk[k];
+        const T inv = T(1) / d;
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+          if (ee[u] < CA && jj[u] > k) {
+            v[u] -= colk[ii[u]] * colk[jj[u]] * inv;
+            if (jj[u] == k + 1) S[ee[u]] = v[u];   // publish the next pivot column
+          }
+        }
+        if (tid == 0) invd[k] = inv;
+        __syncthreads();
+      }
+#pragma unroll
+      for (int u = 0; u < E; ++u) if (ee[u] < CA) S[ee[u]] = v[u];
+    }
+    __syncthreads();
+    tot += clock64() - t0;
+  }
+  if (tid == 0) cyc[0] = tot / reps;
+  for (int i = tid; i < CA; i += NT) out[i] = S[i];
+}
+
+template <typename T>
+void run(int C) {
+  const int CA = C * (C + 3) / 2;
+  // random SPD matrix A = G G^T + C I, augmented with rhs
+  std::vector<double> G(C * C), A(C * C);
+  srand(1);
+  for (auto& g : G) g = (rand() / (double)RAND_MAX) - 0.5;
+  for (int i = 0; i < C; ++i) for (int j = 0; j < C; ++j) { double s = 0; for (int k = 0; k < C; ++k) s += G[i * C + k] * G[j * C + k]; A[i * C + j] = s + (i == j ? C : 0); }
+  std::vector<T> h(CA);
+  for (int j = 0; j < C; ++j) { for (int i = j; i < C; ++i) h[acol(j, C) + i - j] = (T)A[i * C + j]; h[acol(j, C) + C - j] = (T)(j + 1); }
+  T *dA, *dO; long long* dc;
+  cudaMalloc(&dA, CA * sizeof(T)); cudaMalloc(&dO, CA * sizeof(T)); cudaMalloc(&dc, 8);
+  cudaMemcpy(dA, h.data(), CA * sizeof(T), cudaMemcpyHostToDevice);
+  std::vector<T> ref(CA), o(CA);
+  const char* names[] = {"all-threads x4", "1 warp x4", "1 warp lane=row", "all-threads rank-2", "barrier only", "lds-sts-bar", "register-owned"};
+  auto go = [&](auto kern, int v) {
+    kern<<<1, NT>>>(dA, C, 50, dc, dO);
+    long long c; cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(o.data(), dO, CA * sizeof(T), cudaMemcpyDeviceToHost);
+    if (v == 0) ref = o;
+    double err = 0; for (int i = 0; i < CA; ++i) err = fmax(err, fabs((double)o[i] - (double)ref[i]) / (1e-30 + fabs((double)ref[i])));
+    printf("%s C=%d %-20s %6lld cycles  maxrel %.2e  %s\n", sizeof(T) == 4 ? "f32" : "f64", C, names[v], c, err, cudaGetErrorString(cudaGetLastError()));
+  };
+  go(bench<T, 0>, 0); go(bench<T, 1>, 1); go(bench<T, 2>, 2); go(bench<T, 3>, 3); go(bench<T, 4>, 4); go(bench<T, 5>, 5); go(bench<T, 6>, 6);
+}
+
+int main() {
+  run<float>(43); run<double>(43);
+  return 0;
+}

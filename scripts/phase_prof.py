@@ -11,9 +11,10 @@ import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [REPO, os.path.join(REPO, "src")]
-os.environ["MBA_LIB"] = os.path.join(REPO, "paper_2506_05558_b200", "libminiba_prof.so")
+os.environ["MBA_LIB"] = os.environ.get("MBA_PROF_LIB") or os.path.join(REPO, "paper_2506_05558_b200", "libminiba_prof.so")
 
-PHASES = ["setup", "cost0", "point", "jobs", "assemble", "cholesky", "solve+backsub", "trials", "commit"]
+PHASES = ["setup", "cost0", "point", "jobs", "assemble", "cholesky", "solve+backsub", "trials", "commit",
+          "chol_panel_A", "chol_trailing_B"]
 
 
 def main():
@@ -21,6 +22,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--problems", type=int, default=8192)
     ap.add_argument("--precision", default="mixed")
+    ap.add_argument("--kernel", default="auto")
     a = ap.parse_args()
     import torch
     from paper_2506_05558_b200 import _lib, solver
@@ -30,7 +32,8 @@ def main():
     b = make_batch(n, n_cams=c["n_cams"], K=c["K"], outlier_frac=c.get("outlier_frac", 0.0),
                    workers=os.cpu_count())
     db = solver.to_device(solver.pack_synth(b))
-    prm = solver.LmParams(max_iters=c["max_iters"], loss=c["loss"], precision=a.precision)
+    prm = solver.LmParams(max_iters=c["max_iters"], loss=c["loss"], precision=a.precision,
+                          kernel=a.kernel)
     L = _lib.lib()
     buf = torch.zeros(16, dtype=torch.int64, device="cuda")
     L.mba_debug_set_phase_buffer.argtypes = [ct.c_void_p]
@@ -45,7 +48,8 @@ def main():
     cyc = buf.cpu().numpy()[:len(PHASES)].astype(float)
     tot = cyc.sum()
     iters = float(sol.n_iters.sum().item())
-    out = {"config": a.config, "problems": n, "precision": a.precision, "ms": ev[0].elapsed_time(ev[1]),
+    out = {"config": a.config, "problems": n, "precision": a.precision, "kernel": a.kernel,
+           "cluster_env": os.environ.get("MBA_V4_R"), "note": "cycles summed over every CTA of a cluster", "ms": ev[0].elapsed_time(ev[1]),
            "lm_iters": iters,
            "phases": {p: {"frac": c_ / tot, "cycles_per_problem_iter": c_ / iters} for p, c_ in zip(PHASES, cyc)}}
     print(json.dumps(out, indent=1))
