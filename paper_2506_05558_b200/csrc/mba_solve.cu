@@ -2369,16 +2369,17 @@ static int choose_mode(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
   if (cfg->ctas_per_problem < 0) return -cfg->ctas_per_problem;   // forced: 1 warp, 2 CTA, 3 point-wise
   // a few large problems: spread each over the whole GPU (cooperative grid)
   if (d->n_problems <= 8 && d->max_obs >= 4096) return 4;
-  // measured on config 4: CTA-resident 133k problems/s, point-wise
-  // 73k, warp-per-problem 72k (mixed) -> the CTA kernel is the default
-  if (getenv("MBA_AUTO_V4")) return 0;
-  return 2;
+  // batches: the cluster-resident kernel when its shared-memory plan fits
+  // (config 4, f64: 201k problems/s vs 78k for the CTA kernel); the auto
+  // path re-solves plan overflows with the CTA kernel
+  return 0;
 }
 
 template <typename T>
 static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
-  const int mode = choose_mode(d, cfg);
+  int mode = choose_mode(d, cfg);
+  if (mode == 0 && v4::plan_cluster(d, cfg) == 0) mode = 2;   // outside the cluster kernel's envelope
   if (mode == 9 || mode == 0) {
     // cluster-resident kernel; problems whose slices overflow its shared-memory
     // plan are re-solved by the CTA kernel (restricted to flagged problems)
