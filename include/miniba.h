@@ -127,6 +127,12 @@ size_t mba_workspace_bytes(const MbaBatchDesc* desc, const MbaLmConfig* cfg);
 int32_t mba_solve(const MbaBatchDesc* desc, const MbaLmConfig* cfg, const MbaOutputs* out,
                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* Which device path mba_solve takes for this batch and config: the cluster
+ * size R > 0 of the cluster-resident kernel (R CTAs per problem, all scratch in
+ * shared memory; fused backtracking tries 1-4), or -1 warp-per-problem, -2 CTA
+ * per problem, -3 point-wise, -4 whole-GPU cooperative; 0 = not solvable. */
+int32_t mba_solve_plan(const MbaBatchDesc* desc, const MbaLmConfig* cfg);
+
 /* ---- stage entry points (float64), for the reference's internal API ---- */
 
 /* BaProblem.residuals (miniba.py:85-98): r [K][2], p_cam [K][3], bad [K] */

@@ -2445,6 +2445,18 @@ size_t mba_workspace_bytes(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
   return 256 + slot * grid + gextra;
 }
 
+int32_t mba_solve_plan(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
+  if (!d || !cfg || d->n_problems < 1 || d->max_cams < 1 || d->max_obs < 1) return 0;
+  int mode = mba::choose_mode(d, cfg);
+  if (mode == 0 || mode == 9) {
+    const int R = mba::v4::plan_cluster(d, cfg);
+    if (R > 0) return R;
+    if (mode == 9) return 0;
+    mode = 2;
+  }
+  return -mode;
+}
+
 int32_t mba_solve(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o,
                   void* ws, size_t ws_bytes, void* stream) {
   if (!d || !cfg || !o || d->n_problems < 0 || cfg->max_iters < 0) return MBA_ERR_INVALID;

@@ -50,7 +50,7 @@ namespace cg = cooperative_groups;
 namespace mba {
 namespace v4 {
 
-constexpr int NW_MAX = 8;                        // layout bound: warps per CTA
+constexpr int NW_MAX = 16;                       // layout bound: warps per CTA
 #ifndef MBA_NWF_LDL
 #define MBA_NWF_LDL 2
 #endif
@@ -691,6 +691,48 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     out[2] = acc[2];
   };
 
+  // backtracking tries 1..4 (fractions 1/2 .. 1/16) in ONE pass over the
+  // observations: four camera sets / focals / point offsets per observation,
+  // four rank-ordered sums (identical to four separate passes)
+  auto cost4 = [&](const double (&fts)[4], double (&out)[4]) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    constexpr int U = 2;
+    for (int c0 = tid; c0 < nlo; c0 += U * NT) {
+      float4 o[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c0 + u * NT < nlo) o[u] = sobs[c0 + u * NT];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kl = c0 + u * NT;
+        if (kl >= nlo) continue;
+        const int sl = __float_as_int(o[u].w), c = __float_as_int(o[u].z);
+        const double X0 = Xs[3 * sl], X1 = Xs[3 * sl + 1], X2 = Xs[3 * sl + 2];
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+        if (opt_pts) {
+          const T* dp = pf + (size_t)sl * PSTR + 12;
+          d0 = (double)dp[0];
+          d1 = (double)dp[1];
+          d2 = (double)dp[2];
+        }
+        double uu, vv;
+        obs_uv(kl, o[u], uu, vv);
+#pragma unroll
+        for (int bt = 1; bt < kBacktrackTries; ++bt) {
+          const double frac = 1.0 / (double)(1 << bt);
+          const double Xp[3] = {X0 + frac * d0, X1 + frac * d1, X2 + frac * d2};
+          const ProjZ pr = proj_z(Rt + (size_t)(bt * n + c) * 9, tt + (size_t)(bt * n + c) * 3, Xp,
+                                  fts[bt - 1], cx, cy, uu, vv);
+          acc[bt - 1] += rho_e2(pr.ru * pr.ru + pr.rv * pr.rv, delta, loss);
+        }
+      }
+    }
+    block_sum_d<NW, 4>(acc, red);
+    cluster_sum<R, 4>(acc, xch, epoch);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = acc[i];
+  };
+
   double* costs = O.costs + (size_t)b * (max_it + 1);
   double* lambdas = O.lambdas + (size_t)b * max_it;
   uint8_t* accepted = O.accepted + (size_t)b * max_it;
@@ -1108,14 +1150,29 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         }
       }
       __syncthreads();
-      for (int bt = 0; bt < kBacktrackTries; ++bt) {
-        const double frac = ldexp(1.0, -bt);
-        ft = has_f ? f + frac * dc[FI] : f;
-        cost(std::false_type(), Rt + (size_t)bt * n * 9, tt + (size_t)bt * n * 3, ft, frac, opt_pts, tc_);
-        ++tries;
-        if (tc_[0] < cur && isfinite(tc_[0])) {
-          took = bt;
-          break;
+      // try 0 (the full step) alone; if it is rejected, tries 1..4 in one
+      // fused pass. `tries` keeps the reference's count (first accepted try + 1,
+      // or 5), miniba.py:262-276.
+      ft = has_f ? f + dc[FI] : f;
+      cost(std::false_type(), Rt, tt, ft, 1.0, opt_pts, tc_);
+      tries = 1;
+      if (tc_[0] < cur && isfinite(tc_[0])) {
+        took = 0;
+      } else {
+        double fts[4], c4[4];
+#pragma unroll
+        for (int bt = 1; bt < kBacktrackTries; ++bt)
+          fts[bt - 1] = has_f ? f + (1.0 / (double)(1 << bt)) * dc[FI] : f;
+        cost4(fts, c4);
+        tries = kBacktrackTries;
+        for (int bt = 1; bt < kBacktrackTries; ++bt) {
+          if (c4[bt - 1] < cur && isfinite(c4[bt - 1])) {
+            took = bt;
+            tries = bt + 1;
+            tc_[0] = c4[bt - 1];
+            ft = fts[bt - 1];
+            break;
+          }
         }
       }
     } else {
@@ -1226,7 +1283,7 @@ static Plan plan_t(const MbaBatchDesc* d) {
       if (per_sm == 2 && R > 4) continue;
       if (need_bytes<T>(d, R) <= smem_per_cta(per_sm, st)) {
         int nt = per_sm == 2 ? (sizeof(T) == 8 ? 128 : 256) : 256;
-        if (eN == 128 || eN == 256) nt = eN;
+        if (eN == 128 || eN == 256 || (per_sm == 1 && R == 1 && (eN == 384 || eN == 512))) nt = eN;
         if (per_sm == 2 && sizeof(T) == 8) nt = 128;   // 255 registers need 128 threads at 2 CTAs/SM
         return Plan{R, nt, per_sm};
       }
@@ -1300,6 +1357,8 @@ static int launch_prec(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaO
     }
     return MBA_ERR_TOO_LARGE;
   }
+  if (p.nt == 512 && p.R == 1) return launch_t<T, 1, 512, 1>(d, cfg, o, st);
+  if (p.nt == 384 && p.R == 1) return launch_t<T, 1, 384, 1>(d, cfg, o, st);
   switch (p.R) {
     case 1: return launch_t<T, 1, 256, 1>(d, cfg, o, st);
     case 2: return launch_t<T, 2, 256, 1>(d, cfg, o, st);

@@ -285,6 +285,17 @@ def solve(db: DeviceBatch, prm: LmParams, sol: Solution | None = None) -> Soluti
     return sol
 
 
+def plan(db: DeviceBatch, prm: LmParams) -> int:
+    """Device path mba_solve takes (mba_solve_plan): cluster size R > 0 of the
+    cluster-resident kernel, or -1 warp / -2 CTA / -3 point-wise / -4 grid."""
+    sol = Solution.__new__(Solution)
+    for k in ("R", "t", "focal", "points", "costs", "lambdas", "accepted", "evals", "n_iters", "status",
+              "final_stats"):
+        setattr(sol, k, None)
+    d, c, _ = descriptors(db, prm, sol)
+    return int(_lib.lib().mba_solve_plan(ct.byref(d), ct.byref(c)))
+
+
 def fetch(sol: Solution, b: int = 0) -> dict:
     """Copy problem b's results to host in the lm_solve return layout."""
     n = int(sol.n_iters[b].item())

@@ -173,6 +173,59 @@ __global__ void bench(const T* __restrict__ Ain, int C, int reps, long long* cyc
   for (int i = tid; i < CA; i += NT) out[i] = S[i];
 }
 
+
+// register-resident single-warp LDL^T: lane owns rows l and l+32 (row C = rhs),
+// pivot column broadcast by shuffles; CM = compile-time bound on C
+template <typename T, int CM>
+__device__ __forceinline__ void ldl_regs(T* S, T* invd, int C, int lane) {
+  T a[32], b[CM];
+  const int i0 = lane, i1 = lane + 32;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) a[j] = (j <= i0 && i0 <= C && j < C) ? S[acol(j, C) + i0 - j] : T(0);
+#pragma unroll
+  for (int j = 0; j < CM; ++j) b[j] = (i1 <= C && j <= i1 && j < C) ? S[acol(j, C) + i1 - j] : T(0);
+#pragma unroll
+  for (int k = 0; k < CM; ++k) {
+    if (k >= C) break;
+    const T dk = __shfl_sync(0xffffffffu, k < 32 ? a[k < 32 ? k : 0] : b[k], k & 31);
+    const T inv = T(1) / dk;
+    if (lane == 0) invd[k] = inv;
+    const T l0 = (k < 32 && i0 > k) ? a[k < 32 ? k : 0] * inv : T(0);
+    const T l1 = (i1 > k) ? b[k] * inv : T(0);
+#pragma unroll
+    for (int j = k + 1; j < CM; ++j) {
+      if (j >= C) break;
+      const T cjk = __shfl_sync(0xffffffffu, j < 32 ? a[k < 32 ? k : 0] : b[k], j & 31);
+      if (j < 32 && i0 >= j) a[j < 32 ? j : 0] -= l0 * cjk;
+      b[j] -= l1 * cjk;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) if (j <= i0 && i0 <= C && j < C) S[acol(j, C) + i0 - j] = a[j];
+#pragma unroll
+  for (int j = 0; j < CM; ++j) if (i1 <= C && j <= i1 && j < C) S[acol(j, C) + i1 - j] = b[j];
+}
+
+template <typename T, int CM>
+__global__ void bench_regs(const T* __restrict__ Ain, int C, int reps, long long* cyc, T* out) {
+  __shared__ T S[MAXCA], S0[MAXCA], invd[64];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int CA = C * (C + 3) / 2;
+  for (int i = tid; i < CA; i += NT) S0[i] = Ain[i];
+  __syncthreads();
+  long long tot = 0;
+  for (int r = 0; r < reps; ++r) {
+    for (int i = tid; i < CA; i += NT) S[i] = S0[i];
+    __syncthreads();
+    long long t0 = clock64();
+    if (wid == 0) ldl_regs<T, CM>(S, invd, C, lane);
+    __syncthreads();
+    tot += clock64() - t0;
+  }
+  if (tid == 0) cyc[0] = tot / reps;
+  for (int i = tid; i < CA; i += NT) out[i] = S[i];
+}
+
 template <typename T>
 void run(int C) {
   const int CA = C * (C + 3) / 2;
@@ -187,7 +240,7 @@ void run(int C) {
   cudaMalloc(&dA, CA * sizeof(T)); cudaMalloc(&dO, CA * sizeof(T)); cudaMalloc(&dc, 8);
   cudaMemcpy(dA, h.data(), CA * sizeof(T), cudaMemcpyHostToDevice);
   std::vector<T> ref(CA), o(CA);
-  const char* names[] = {"all-threads x4", "1 warp x4", "1 warp lane=row", "all-threads rank-2", "barrier only", "lds-sts-bar", "register-owned"};
+  const char* names[] = {"all-threads x4", "1 warp x4", "1 warp lane=row", "all-threads rank-2", "barrier only", "lds-sts-bar", "register-owned", "warp registers CM=43", "warp registers CM=49"};
   auto go = [&](auto kern, int v) {
     kern<<<1, NT>>>(dA, C, 50, dc, dO);
     long long c; cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
@@ -196,7 +249,7 @@ void run(int C) {
     double err = 0; for (int i = 0; i < CA; ++i) err = fmax(err, fabs((double)o[i] - (double)ref[i]) / (1e-30 + fabs((double)ref[i])));
     printf("%s C=%d %-20s %6lld cycles  maxrel %.2e  %s\n", sizeof(T) == 4 ? "f32" : "f64", C, names[v], c, err, cudaGetErrorString(cudaGetLastError()));
   };
-  go(bench<T, 0>, 0); go(bench<T, 1>, 1); go(bench<T, 2>, 2); go(bench<T, 3>, 3); go(bench<T, 4>, 4); go(bench<T, 5>, 5); go(bench<T, 6>, 6);
+  go(bench<T, 0>, 0); go(bench<T, 1>, 1); go(bench<T, 2>, 2); go(bench<T, 3>, 3); go(bench<T, 4>, 4); go(bench<T, 5>, 5); go(bench<T, 6>, 6); go(bench_regs<T, 43>, 7); go(bench_regs<T, 49>, 8);
 }
 
 int main() {
