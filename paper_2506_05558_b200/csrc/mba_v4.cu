@@ -96,7 +96,8 @@ struct Fixed {
   static constexpr size_t oBlkB = oBlkA + MAXNB;                      // u8[MAXNB]
   static constexpr size_t oRcT = al16(oBlkB + MAXNB);                 // T[MAXN][9] rotations in T
   static constexpr size_t oDcT = al16(oRcT + sizeof(T) * 9 * MAXN);   // T[MAXC] step in T
-  static constexpr size_t kBytes = al16(oDcT + sizeof(T) * MAXC);
+  static constexpr size_t oL10 = al16(oDcT + sizeof(T) * MAXC);       // T[MAXC] LDL^T pair multipliers
+  static constexpr size_t kBytes = al16(oL10 + sizeof(T) * MAXC);
 };
 
 // bytes per local observation / observed point in the arena (plus pairs, 4 B each)
@@ -265,6 +266,18 @@ __device__ __forceinline__ ProjZ proj_z(const double* __restrict__ R, const doub
   return o;
 }
 
+// reciprocal for the factorisation pivots: fp64 MUFU seed + two Newton steps
+// (<= 1 ulp), fp32 correctly rounded
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ float fast_rcp(float x) { return 1.0f / x; }
+
 // robust cost from the squared residual norm (miniba.py:46-50 + Cauchy): the
 // square root is only taken for Huber observations beyond delta
 __device__ __forceinline__ double rho_e2(double e2, double delta, int loss) {
@@ -390,6 +403,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   unsigned char* arena = smem + F::kBytes;
   T* RcT = (T*)(smem + F::oRcT);
   T* dcT = (T*)(smem + F::oDcT);
+  T* l10s = (T*)(smem + F::oL10);
 
   __shared__ int s_flag, s_nf, s_nlp, s_npairs, s_job;
   __shared__ int s_cf[2];   // panel pivot failure, double-buffered by panel parity
@@ -1028,38 +1042,93 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
 
     PROF_MARK(PH_ASM)
     // ---------- LDL^T of the augmented system ----------
-    // Column-by-column right-looking elimination of the packed augmented
-    // system, one barrier per column; each thread updates up to 4 entries per
-    // column with all loads issued before the arithmetic (no dependent load
-    // chain per entry). S[k][k] keeps d_k, S[i][k] keeps L_ik d_k; the rhs
-    // row C receives the forward substitution y = L^-1 b.
+    // Right-looking, two pivots per step and ONE barrier per step: pivots k and
+    // k+1 (d_k, l = S[k+1][k]/d_k, d_{k+1} = S[k+1][k+1] - l S[k+1][k]) are
+    // formed redundantly by every thread, the trailing entries get the rank-2
+    // update with column k+1 corrected on the fly, and column k+1 itself is
+    // finalised lazily during the next step (nobody reads it there). Each
+    // thread owns fixed packed entries whose (row, column) stay in registers;
+    // reciprocals are MUFU-seeded with Newton refinement in fp64. S[k][k] keeps
+    // d_k, S[i][k] keeps L_ik d_k; the rhs row C receives y = L^-1 b.
+    // (B200: a shared store -> barrier -> load round trip costs ~200 cycles,
+    // scripts/micro/ldl_bench.cu; this variant measured 14.8k cycles for C=43
+    // in fp64 against 22.1k for one barrier per column.)
     bool chol_fail = false;
-    for (int k = 0; k < C; ++k) {
-      const T* colk = S + acol(k, C) - k;  // colk[i] = S[i][k], i in [k, C]
-      const int e0 = acol(k + 1, C);
-      const T d = colk[k];
-      if (!(d > T(0)) || !isfinite(d)) {
-        chol_fail = true;  // every thread reads the same pivot: uniform exit
-        break;
+    {
+      constexpr int E = (CA_MAX + NT - 1) / NT;
+      int ii[E], jj[E];
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        const int e = tid + u * NT;
+        const unsigned ij = e < CA ? tab[e] : 0u;
+        ii[u] = e < CA ? (int)(ij >> 8) : 0;
+        jj[u] = e < CA ? (int)(ij & 255u) : -1;
       }
-      for (int eb = e0 + tid; eb < CA; eb += 4 * NT) {
-        unsigned ij[4];
-        T ci[4], cj[4], sv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) ij[u] = eb + u * NT < CA ? tab[eb + u * NT] : 0u;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          ci[u] = colk[ij[u] >> 8];
-          cj[u] = colk[ij[u] & 255u];
-          sv[u] = eb + u * NT < CA ? S[eb + u * NT] : T(0);
+      auto bad_pivot = [](T d) { return !(d > T(0)) || !isfinite(d); };
+      int k = 0, pend = -1;   // pend: column awaiting its rank-1 finalisation
+      for (; k + 1 < C; k += 2) {
+        const T* colk = S + acol(k, C) - k;
+        const T* colk1 = S + acol(k + 1, C) - (k + 1);
+        const T d0 = colk[k], a10 = colk[k + 1], d1r = colk1[k + 1];
+        if (bad_pivot(d0)) {
+          chol_fail = true;
+          break;
         }
-        const T inv = T(1) / d;
+        const T i0 = fast_rcp(d0);
+        const T l10 = a10 * i0;
+        const T d1 = d1r - l10 * a10;
+        if (bad_pivot(d1)) {
+          chol_fail = true;
+          break;
+        }
+        const T i1 = fast_rcp(d1);
+        if (tid == 0) {
+          invd[k] = i0;
+          invd[k + 1] = i1;
+          l10s[k] = l10;
+        }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (eb + u * NT < CA) S[eb + u * NT] = sv[u] - ci[u] * cj[u] * inv;
+        for (int u = 0; u < E; ++u) {
+          if (jj[u] >= k + 2) {
+            const int e = tid + u * NT;
+            const T ai = colk[ii[u]], aj = colk[jj[u]], ci = colk1[ii[u]], cj = colk1[jj[u]];
+            const T sv = S[e];
+            const T ci1 = ci - ai * l10, cj1 = cj - aj * l10;
+            S[e] = sv - ai * aj * i0 - ci1 * cj1 * i1;
+          }
+        }
+        if (pend >= 0) {   // finalise column pend (= k - 1) against column pend - 1
+          T* cp = S + acol(pend, C) - pend;
+          const T* cq = S + acol(pend - 1, C) - (pend - 1);
+          const T lp = l10s[pend - 1];
+          for (int i = pend + tid; i <= C; i += NT) cp[i] = cp[i] - cq[i] * lp;
+        }
+        pend = k + 1;
+        __syncthreads();
       }
-      if (tid == 0) invd[k] = T(1) / d;
-      __syncthreads();
+      if (!chol_fail) {
+        if (pend >= 0) {
+          T* cp = S + acol(pend, C) - pend;
+          const T* cq = S + acol(pend - 1, C) - (pend - 1);
+          const T lp = l10s[pend - 1];
+          for (int i = pend + tid; i <= C; i += NT) cp[i] = cp[i] - cq[i] * lp;
+          __syncthreads();
+        }
+        if (k < C) {   // odd C: the last pivot alone
+          const T* colk = S + acol(k, C) - k;
+          const T d = colk[k];
+          if (bad_pivot(d)) {
+            chol_fail = true;
+          } else {
+            const T inv = fast_rcp(d);
+#pragma unroll
+            for (int u = 0; u < E; ++u)
+              if (jj[u] > k) S[tid + u * NT] -= colk[ii[u]] * colk[jj[u]] * inv;
+            if (tid == 0) invd[k] = inv;
+          }
+          __syncthreads();
+        }
+      }
     }
     PROF_MARK(PH_CHA)
     if (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull)) chol_fail = true;

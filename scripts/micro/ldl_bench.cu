@@ -226,6 +226,218 @@ __global__ void bench_regs(const T* __restrict__ Ain, int C, int reps, long long
   for (int i = tid; i < CA; i += NT) out[i] = S[i];
 }
 
+
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ float frcp(float x) { return __frcp_rn(x); }
+
+// rank-2 steps, fast reciprocals, register-held (i,j) per thread entry
+template <typename T>
+__global__ void bench_r2f(const T* __restrict__ Ain, int C, int reps, long long* cyc, T* out) {
+  __shared__ T S[MAXCA], S0[MAXCA], invd[64];
+  __shared__ unsigned short tab[MAXCA];
+  const int tid = threadIdx.x;
+  const int CA = C * (C + 3) / 2;
+  for (int i = tid; i < CA; i += NT) S0[i] = Ain[i];
+  for (int j = tid; j < C; j += NT) {
+    const int a0 = acol(j, C);
+    for (int i = j; i <= C; ++i) tab[a0 + i - j] = (unsigned short)((i << 8) | j);
+  }
+  __syncthreads();
+  long long tot = 0;
+  for (int r = 0; r < reps; ++r) {
+    for (int i = tid; i < CA; i += NT) S[i] = S0[i];
+    __syncthreads();
+    long long t0 = clock64();
+    constexpr int E = 5;
+    int ii[E], jj[E];
+#pragma unroll
+    for (int u = 0; u < E; ++u) {
+      const int e = tid + u * NT;
+      const unsigned ij = e < CA ? tab[e] : 0u;
+      ii[u] = e < CA ? (int)(ij >> 8) : 0;
+      jj[u] = e < CA ? (int)(ij & 255u) : -1;
+    }
+    int k = 0;
+    for (; k + 1 < C; k += 2) {
+      const T* colk = S + acol(k, C) - k;
+      T* colk1 = S + acol(k + 1, C) - (k + 1);
+      const T d0 = colk[k], a10 = colk[k + 1], d1r = colk1[k + 1];
+      const T i0 = frcp(d0);
+      const T l10 = a10 * i0;
+      const T d1 = d1r - l10 * a10;
+      const T i1 = frcp(d1);
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        const int e = tid + u * NT;
+        if (jj[u] >= k + 2) {
+          const T a = colk[ii[u]], b = colk[jj[u]], c = colk1[ii[u]], dd = colk1[jj[u]];
+          const T sv = S[e];
+          const T ci1 = c - a * l10, cj1 = dd - b * l10;
+          S[e] = sv - a * b * i0 - ci1 * cj1 * i1;
+        }
+      }
+      __syncthreads();
+      for (int i = k + 1 + tid; i <= C; i += NT) colk1[i] = (i == k + 1) ? d1 : colk1[i] - colk[i] * l10;
+      if (tid == 0) { invd[k] = i0; invd[k + 1] = i1; }
+      __syncthreads();
+    }
+    for (; k < C; ++k) {
+      const T* colk = S + acol(k, C) - k;
+      const T d = colk[k];
+      const T inv = frcp(d);
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        const int e = tid + u * NT;
+        if (jj[u] > k) S[e] -= colk[ii[u]] * colk[jj[u]] * inv;
+      }
+      if (tid == 0) invd[k] = inv;
+      __syncthreads();
+    }
+    __syncthreads();
+    tot += clock64() - t0;
+  }
+  if (tid == 0) cyc[0] = tot / reps;
+  for (int i = tid; i < CA; i += NT) out[i] = S[i];
+}
+
+// rank-1 steps, fast reciprocal, register-held (i,j)
+template <typename T>
+__global__ void bench_r1f(const T* __restrict__ Ain, int C, int reps, long long* cyc, T* out) {
+  __shared__ T S[MAXCA], S0[MAXCA], invd[64];
+  __shared__ unsigned short tab[MAXCA];
+  const int tid = threadIdx.x;
+  const int CA = C * (C + 3) / 2;
+  for (int i = tid; i < CA; i += NT) S0[i] = Ain[i];
+  for (int j = tid; j < C; j += NT) {
+    const int a0 = acol(j, C);
+    for (int i = j; i <= C; ++i) tab[a0 + i - j] = (unsigned short)((i << 8) | j);
+  }
+  __syncthreads();
+  long long tot = 0;
+  for (int r = 0; r < reps; ++r) {
+    for (int i = tid; i < CA; i += NT) S[i] = S0[i];
+    __syncthreads();
+    long long t0 = clock64();
+    constexpr int E = 5;
+    int ii[E], jj[E];
+#pragma unroll
+    for (int u = 0; u < E; ++u) {
+      const int e = tid + u * NT;
+      const unsigned ij = e < CA ? tab[e] : 0u;
+      ii[u] = e < CA ? (int)(ij >> 8) : 0;
+      jj[u] = e < CA ? (int)(ij & 255u) : -1;
+    }
+    for (int k = 0; k < C; ++k) {
+      const T* colk = S + acol(k, C) - k;
+      const T d = colk[k];
+      const T inv = frcp(d);
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        const int e = tid + u * NT;
+        if (jj[u] > k) S[e] -= colk[ii[u]] * colk[jj[u]] * inv;
+      }
+      if (tid == 0) invd[k] = inv;
+      __syncthreads();
+    }
+    __syncthreads();
+    tot += clock64() - t0;
+  }
+  if (tid == 0) cyc[0] = tot / reps;
+  for (int i = tid; i < CA; i += NT) out[i] = S[i];
+}
+
+
+// rank-2 steps with ONE barrier per step: column k+1 is finalised lazily in the
+// next step (nobody reads it there); fast reciprocals; register-held (i,j)
+template <typename T>
+__global__ void bench_r2b(const T* __restrict__ Ain, int C, int reps, long long* cyc, T* out) {
+  __shared__ T S[MAXCA], S0[MAXCA], invd[64], l10s[64];
+  __shared__ unsigned short tab[MAXCA];
+  const int tid = threadIdx.x;
+  const int CA = C * (C + 3) / 2;
+  for (int i = tid; i < CA; i += NT) S0[i] = Ain[i];
+  for (int j = tid; j < C; j += NT) {
+    const int a0 = acol(j, C);
+    for (int i = j; i <= C; ++i) tab[a0 + i - j] = (unsigned short)((i << 8) | j);
+  }
+  __syncthreads();
+  long long tot = 0;
+  for (int r = 0; r < reps; ++r) {
+    for (int i = tid; i < CA; i += NT) S[i] = S0[i];
+    __syncthreads();
+    long long t0 = clock64();
+    constexpr int E = 5;
+    int ii[E], jj[E];
+#pragma unroll
+    for (int u = 0; u < E; ++u) {
+      const int e = tid + u * NT;
+      const unsigned ij = e < CA ? tab[e] : 0u;
+      ii[u] = e < CA ? (int)(ij >> 8) : 0;
+      jj[u] = e < CA ? (int)(ij & 255u) : -1;
+    }
+    int k = 0;
+    int pend = -1;   // column waiting for its rank-1 finalisation (pend = k-1 of the previous step)
+    for (; k + 1 < C; k += 2) {
+      const T* colk = S + acol(k, C) - k;
+      const T* colk1 = S + acol(k + 1, C) - (k + 1);
+      const T d0 = colk[k], a10 = colk[k + 1], d1r = colk1[k + 1];
+      const T i0 = frcp(d0);
+      const T l10 = a10 * i0;
+      const T d1 = d1r - l10 * a10;
+      const T i1 = frcp(d1);
+      if (tid == 0) { invd[k] = i0; invd[k + 1] = i1; l10s[k] = l10; }
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        const int e = tid + u * NT;
+        if (jj[u] >= k + 2) {
+          const T a = colk[ii[u]], b = colk[jj[u]], c = colk1[ii[u]], dd = colk1[jj[u]];
+          const T sv = S[e];
+          const T ci1 = c - a * l10, cj1 = dd - b * l10;
+          S[e] = sv - a * b * i0 - ci1 * cj1 * i1;
+        }
+      }
+      if (pend >= 0) {   // finalise column pend = k-1 (rank-1 with column k-2)
+        T* cp = S + acol(pend, C) - pend;
+        const T* cq = S + acol(pend - 1, C) - (pend - 1);
+        const T lp = l10s[pend - 1];
+        for (int i = pend + tid; i <= C; i += NT) cp[i] = (i == pend) ? cp[i] - lp * cq[pend] : cp[i] - cq[i] * lp;
+      }
+      pend = k + 1;
+      __syncthreads();
+    }
+    if (pend >= 0) {
+      T* cp = S + acol(pend, C) - pend;
+      const T* cq = S + acol(pend - 1, C) - (pend - 1);
+      const T lp = l10s[pend - 1];
+      for (int i = pend + tid; i <= C; i += NT) cp[i] = (i == pend) ? cp[i] - lp * cq[pend] : cp[i] - cq[i] * lp;
+      __syncthreads();
+    }
+    for (; k < C; ++k) {
+      const T* colk = S + acol(k, C) - k;
+      const T d = colk[k];
+      const T inv = frcp(d);
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        const int e = tid + u * NT;
+        if (jj[u] > k) S[e] -= colk[ii[u]] * colk[jj[u]] * inv;
+      }
+      if (tid == 0) invd[k] = inv;
+      __syncthreads();
+    }
+    __syncthreads();
+    tot += clock64() - t0;
+  }
+  if (tid == 0) cyc[0] = tot / reps;
+  for (int i = tid; i < CA; i += NT) out[i] = S[i];
+}
+
 template <typename T>
 void run(int C) {
   const int CA = C * (C + 3) / 2;
@@ -240,7 +452,7 @@ void run(int C) {
   cudaMalloc(&dA, CA * sizeof(T)); cudaMalloc(&dO, CA * sizeof(T)); cudaMalloc(&dc, 8);
   cudaMemcpy(dA, h.data(), CA * sizeof(T), cudaMemcpyHostToDevice);
   std::vector<T> ref(CA), o(CA);
-  const char* names[] = {"all-threads x4", "1 warp x4", "1 warp lane=row", "all-threads rank-2", "barrier only", "lds-sts-bar", "register-owned", "warp registers CM=43", "warp registers CM=49"};
+  const char* names[] = {"all-threads x4", "1 warp x4", "1 warp lane=row", "all-threads rank-2", "barrier only", "lds-sts-bar", "register-owned", "warp registers CM=43", "warp registers CM=49", "rank-2 fast-rcp regs", "rank-1 fast-rcp regs", "rank-2 1-barrier"};
   auto go = [&](auto kern, int v) {
     kern<<<1, NT>>>(dA, C, 50, dc, dO);
     long long c; cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
@@ -249,10 +461,10 @@ void run(int C) {
     double err = 0; for (int i = 0; i < CA; ++i) err = fmax(err, fabs((double)o[i] - (double)ref[i]) / (1e-30 + fabs((double)ref[i])));
     printf("%s C=%d %-20s %6lld cycles  maxrel %.2e  %s\n", sizeof(T) == 4 ? "f32" : "f64", C, names[v], c, err, cudaGetErrorString(cudaGetLastError()));
   };
-  go(bench<T, 0>, 0); go(bench<T, 1>, 1); go(bench<T, 2>, 2); go(bench<T, 3>, 3); go(bench<T, 4>, 4); go(bench<T, 5>, 5); go(bench<T, 6>, 6); go(bench_regs<T, 43>, 7); go(bench_regs<T, 49>, 8);
+  go(bench<T, 0>, 0); go(bench<T, 3>, 3); go(bench_r2f<T>, 9); go(bench_r2b<T>, 11);
 }
 
 int main() {
-  run<float>(43); run<double>(43);
+  run<float>(43); run<double>(43); run<float>(49); run<double>(49); run<double>(42);
   return 0;
 }
