@@ -587,6 +587,23 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       }
     }
     __syncthreads();
+    // per point, where each camera's observation sits: nibble c of cpos[sl] is
+    // 0 (camera c does not see the point), 1..14 (offset + 1 of its only
+    // observation) or 15 (several observations / long track: scan). Scratch in
+    // the (not yet used) Jacobian area.
+    unsigned* cpos = reinterpret_cast<unsigned*>(jac);
+    for (int sl = tid; sl < nlp; sl += NT) {
+      unsigned m = 0u;
+      const int j0 = ptr[sl], j1 = ptr[sl + 1];
+      for (int j = j0; j < j1; ++j) {
+        const int c = __float_as_int(sobs[j].z), sh = 4 * c;
+        const unsigned cur = (m >> sh) & 15u;
+        const unsigned v = (cur == 0u && j - j0 < 14) ? (unsigned)(j - j0 + 1) : 15u;
+        m = (m & ~(15u << sh)) | (v << sh);
+      }
+      cpos[sl] = m;
+    }
+    __syncthreads();
     // co-observation pair lists per free camera block (a <= b): count, scan, fill
     for (int pass = 0; pass < 2; ++pass) {
       for (int blk = wid; blk < nb; blk += NW) {
@@ -596,18 +613,28 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         for (int q0 = cam_ptr[ca]; q0 < q1; q0 += 32) {
           const int q = q0 + lane;
           int i = -1, j0 = 0, j1 = 0, m = 0;
+          unsigned nib = 0u;
           if (q < q1) {
             i = perm[q];
             const int sl = __float_as_int(sobs[i].w);
             j0 = ptr[sl];
             j1 = ptr[sl + 1];
-            for (int j = j0; j < j1; ++j) m += __float_as_int(sobs[j].z) == cbb;
+            nib = (cpos[sl] >> (4 * cbb)) & 15u;
+            if (nib == 15u) {
+              for (int j = j0; j < j1; ++j) m += __float_as_int(sobs[j].z) == cbb;
+            } else {
+              m = nib != 0u;
+            }
           }
           if (pass) {
             const int inc = warp_incl_scan(m, lane);
             int pos = basep + inc - m;
-            for (int j = j0; j < j1 && m; ++j)
-              if (__float_as_int(sobs[j].z) == cbb) pairs[pos++] = ((unsigned)i << 16) | (unsigned)j;
+            if (nib == 15u) {
+              for (int j = j0; j < j1 && m; ++j)
+                if (__float_as_int(sobs[j].z) == cbb) pairs[pos++] = ((unsigned)i << 16) | (unsigned)j;
+            } else if (m) {
+              pairs[pos] = ((unsigned)i << 16) | (unsigned)(j0 + (int)nib - 1);
+            }
           }
           basep += warp_sum(m);
         }
