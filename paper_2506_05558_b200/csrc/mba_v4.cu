@@ -66,7 +66,7 @@ constexpr int CA_MAX = MAXC * (MAXC + 3) / 2;    // augmented packed size
 template <typename T>
 __host__ __device__ constexpr int jstr() { return sizeof(T) == 8 ? 3 : 5; }
 constexpr int PSTR = 15;   // per point: iL00 L10 iL11 L20 L21 iL22 z0..2 yf0..2 dp0..2
-constexpr int UST = 45;    // camera job: U_aa(21) U_af(6) g_a(6) SYf(6) SYz(6)
+constexpr int UST = 51;    // camera job: U_aa - sum_self Y Y^T (21) U_af(6) g_a(6) SYf(6) SYz(6) diag U_aa(6)
 constexpr int JOB_PAIR0 = MAXN * UST;
 constexpr int JOB_PART = JOB_PAIR0 + MAXNB * 36;
 constexpr int JOB_OUT = JOB_PART + 4;
@@ -406,7 +406,8 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   T* l10s = (T*)(smem + F::oL10);
 
   __shared__ int s_flag, s_nf, s_nlp, s_npairs, s_job;
-  __shared__ int s_cf[2];   // panel pivot failure, double-buffered by panel parity
+  __shared__ int s_cf[2];   // pivot failure flags
+  __shared__ unsigned char s_jorder[MAXN + MAXNB];   // job queue order: longest first
   __shared__ int s_wtot[NW_MAX];
   int epoch = 0;
   PROF_DECL
@@ -619,11 +620,12 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
             const int sl = __float_as_int(sobs[i].w);
             j0 = ptr[sl];
             j1 = ptr[sl + 1];
+            // self pairs (j == i) are folded into the camera jobs
             nib = (cpos[sl] >> (4 * cbb)) & 15u;
             if (nib == 15u) {
-              for (int j = j0; j < j1; ++j) m += __float_as_int(sobs[j].z) == cbb;
+              for (int j = j0; j < j1; ++j) m += __float_as_int(sobs[j].z) == cbb && j != i;
             } else {
-              m = nib != 0u;
+              m = nib != 0u && j0 + (int)nib - 1 != i;
             }
           }
           if (pass) {
@@ -631,7 +633,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
             int pos = basep + inc - m;
             if (nib == 15u) {
               for (int j = j0; j < j1 && m; ++j)
-                if (__float_as_int(sobs[j].z) == cbb) pairs[pos++] = ((unsigned)i << 16) | (unsigned)j;
+                if (__float_as_int(sobs[j].z) == cbb && j != i) pairs[pos++] = ((unsigned)i << 16) | (unsigned)j;
             } else if (m) {
               pairs[pos] = ((unsigned)i << 16) | (unsigned)(j0 + (int)nib - 1);
             }
@@ -653,6 +655,25 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
           break;
         }
       }
+    }
+  }
+  // job queue order, longest first (results do not depend on the order)
+  if (tid == 0 && !overflow) {
+    int w[MAXN + MAXNB];
+    const int nj = nf + nb;
+    for (int q = 0; q < nj; ++q) {
+      w[q] = q < nf ? 3 * (cam_ptr[cslot[q] + 1] - cam_ptr[cslot[q]]) / 2
+                    : blk_off[q - nf + 1] - blk_off[q - nf];
+      s_jorder[q] = (unsigned char)q;
+    }
+    for (int q = 1; q < nj; ++q) {   // insertion sort, descending, stable
+      const unsigned char jq = s_jorder[q];
+      int r = q - 1;
+      while (r >= 0 && w[s_jorder[r]] < w[jq]) {
+        s_jorder[r + 1] = s_jorder[r];
+        --r;
+      }
+      s_jorder[r + 1] = jq;
     }
   }
   // packed position -> (row, col) table of the augmented system
@@ -880,6 +901,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       if (lane == 0) jb = atomicAdd(&s_job, 1);
       jb = __shfl_sync(0xffffffffu, jb, 0);
       if (jb >= nf + nb) break;
+      jb = s_jorder[jb];
       if (jb < nf) {
         const int s = jb, c = cslot[s];
         T Rt9[9];
@@ -915,14 +937,11 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
           }
           T a[12];
           expand_A(J0, J1, J2, v0, v1, v2, a);
-          int idx = 0;
+          // self co-observation product of the diagonal block, folded in:
+          // U_aa - Y_i Y_i^T = A^T A - A^T (Q Q^T) A = A^T (A - P), P = (Q Q^T) A
+          T p[12];
 #pragma unroll
-          for (int r = 0; r < 6; ++r) {
-#pragma unroll
-            for (int cc = 0; cc <= r; ++cc) acc[idx++] += a[r] * a[cc] + a[6 + r] * a[6 + cc];
-            acc[21 + r] += a[r] * F0 + a[6 + r] * F1;
-            acc[27 + r] += a[r] * r0 + a[6 + r] * r1;
-          }
+          for (int i = 0; i < 12; ++i) p[i] = T(0);
           if (opt_pts) {
             const T* pw = pf + (size_t)sl * PSTR;
             T qv[6];
@@ -931,16 +950,35 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
             const T qf1 = qv[3] * pw[9] + qv[4] * pw[10] + qv[5] * pw[11];
             const T qz0 = qv[0] * pw[6] + qv[1] * pw[7] + qv[2] * pw[8];
             const T qz1 = qv[3] * pw[6] + qv[4] * pw[7] + qv[5] * pw[8];
+            const T m00 = qv[0] * qv[0] + qv[1] * qv[1] + qv[2] * qv[2];
+            const T m01 = qv[0] * qv[3] + qv[1] * qv[4] + qv[2] * qv[5];
+            const T m11 = qv[3] * qv[3] + qv[4] * qv[4] + qv[5] * qv[5];
 #pragma unroll
             for (int r = 0; r < 6; ++r) {
               acc[33 + r] += a[r] * qf0 + a[6 + r] * qf1;
               acc[39 + r] += a[r] * qz0 + a[6 + r] * qz1;
+              p[r] = m00 * a[r] + m01 * a[6 + r];
+              p[6 + r] = m01 * a[r] + m11 * a[6 + r];
             }
+          }
+          int idx = 0;
+#pragma unroll
+          for (int r = 0; r < 6; ++r) {
+#pragma unroll
+            for (int cc = 0; cc <= r; ++cc) acc[idx++] += a[r] * (a[cc] - p[cc]) + a[6 + r] * (a[6 + cc] - p[6 + cc]);
+            acc[21 + r] += a[r] * F0 + a[6 + r] * F1;
+            acc[27 + r] += a[r] * r0 + a[6 + r] * r1;
+            acc[45 + r] += a[r] * a[r] + a[6 + r] * a[6 + r];
           }
         }
         warp_reduce_to<T, UST>(acc, job + s * UST, lane);
       } else {
         const int blk = jb - nf;
+        if (blk_off[blk + 1] == blk_off[blk]) {   // no co-observations (e.g. diagonal blocks)
+          T* o = job + JOB_PAIR0 + blk * 36;
+          for (int i = lane; i < 36; i += 32) o[i] = T(0);
+          continue;
+        }
         const int ca = cslot[blk_a[blk]], cbb = cslot[blk_b[blk]];
         T Ra[9], Rb[9];
 #pragma unroll
@@ -1050,8 +1088,11 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         val = T(0);
         if (sa == sb) {
           const int r = ri, cc = rj;  // r >= cc
-          T ud = jsum_at(sa * UST + r * (r + 1) / 2 + cc);
-          if (r == cc) ud += tlam * (ud > T(kDiagFloor) ? ud : T(kDiagFloor));
+          T ud = jsum_at(sa * UST + r * (r + 1) / 2 + cc);   // U_aa - sum_self Y Y^T
+          if (r == cc) {
+            const T u0 = jsum_at(sa * UST + 45 + r);         // U_aa diagonal (damping, miniba.py:190)
+            ud += tlam * (u0 > T(kDiagFloor) ? u0 : T(kDiagFloor));
+          }
           val = ud;
           if (opt_pts) {
             const int q = sa * nf - sa * (sa - 1) / 2;   // block (sa, sa)
