@@ -1419,7 +1419,10 @@ static Plan plan_t(const MbaBatchDesc* d) {
       if (eP && per_sm != eP) continue;
       if (per_sm == 2 && R > 4) continue;
       if (need_bytes<T>(d, R) <= smem_per_cta(per_sm, st)) {
-        int nt = per_sm == 2 ? (sizeof(T) == 8 ? 128 : 256) : 256;
+        // one problem per SM: fp32 arithmetic fits 512 threads in 128 registers
+        // (config 4 mixed: 324k problems/s at 512 vs 283k at 256); fp64 needs
+        // the register room of 256 threads
+        int nt = per_sm == 2 ? (sizeof(T) == 8 ? 128 : 256) : (sizeof(T) == 4 && R == 1 ? 512 : 256);
         if (eN == 128 || eN == 256 || (per_sm == 1 && R == 1 && (eN == 384 || eN == 512))) nt = eN;
         if (per_sm == 2 && sizeof(T) == 8) nt = 128;   // 255 registers need 128 threads at 2 CTAs/SM
         return Plan{R, nt, per_sm};
