@@ -657,23 +657,19 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       }
     }
   }
-  // job queue order, longest first (results do not depend on the order)
-  if (tid == 0 && !overflow) {
-    int w[MAXN + MAXNB];
+  // job queue order, longest first (results do not depend on the order):
+  // job q's rank = number of jobs that are heavier (ties by index)
+  if (!overflow) {
+    __shared__ int s_w[MAXN + MAXNB];
     const int nj = nf + nb;
-    for (int q = 0; q < nj; ++q) {
-      w[q] = q < nf ? 3 * (cam_ptr[cslot[q] + 1] - cam_ptr[cslot[q]]) / 2
-                    : blk_off[q - nf + 1] - blk_off[q - nf];
-      s_jorder[q] = (unsigned char)q;
-    }
-    for (int q = 1; q < nj; ++q) {   // insertion sort, descending, stable
-      const unsigned char jq = s_jorder[q];
-      int r = q - 1;
-      while (r >= 0 && w[s_jorder[r]] < w[jq]) {
-        s_jorder[r + 1] = s_jorder[r];
-        --r;
-      }
-      s_jorder[r + 1] = jq;
+    for (int q = tid; q < nj; q += NT)
+      s_w[q] = q < nf ? 3 * (cam_ptr[cslot[q] + 1] - cam_ptr[cslot[q]]) / 2
+                      : blk_off[q - nf + 1] - blk_off[q - nf];
+    __syncthreads();
+    for (int q = tid; q < nj; q += NT) {
+      int rk = 0;
+      for (int r = 0; r < nj; ++r) rk += s_w[r] > s_w[q] || (s_w[r] == s_w[q] && r < q);
+      s_jorder[rk] = (unsigned char)q;
     }
   }
   // packed position -> (row, col) table of the augmented system
