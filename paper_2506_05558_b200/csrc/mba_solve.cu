@@ -2367,12 +2367,15 @@ static int launch_warp(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaO
 // CTA per problem (scratch in shared memory when it fits).
 static int choose_mode(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
   if (cfg->ctas_per_problem < 0) return -cfg->ctas_per_problem;   // forced: 1 warp, 2 CTA, 3 point-wise
-  // a few large problems: spread each over the whole GPU (cooperative grid)
+  // the cluster-resident kernel whenever its shared-memory plan fits (<= 8
+  // cameras): config 4 f64 250k problems/s vs 78k for the CTA kernel; a single
+  // config-2 problem (K = 20k) in 0.44 ms on a 16-CTA cluster vs 2.43 ms for
+  // the whole-GPU cooperative kernel. Plan overflows are re-solved by the CTA
+  // kernel.
+  if (v4::plan_cluster(d, cfg) > 0) return 0;
+  // otherwise a few large problems spread over the whole GPU (cooperative grid)
   if (d->n_problems <= 8 && d->max_obs >= 4096) return 4;
-  // batches: the cluster-resident kernel when its shared-memory plan fits
-  // (config 4, f64: 201k problems/s vs 78k for the CTA kernel); the auto
-  // path re-solves plan overflows with the CTA kernel
-  return 0;
+  return 2;
 }
 
 template <typename T>

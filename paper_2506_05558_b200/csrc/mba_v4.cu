@@ -900,9 +900,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       jb = s_jorder[jb];
       if (jb < nf) {
         const int s = jb, c = cslot[s];
-        T Rt9[9];
-#pragma unroll
-        for (int i = 0; i < 9; ++i) Rt9[i] = RcT[9 * c + i];
+        const T* Rt9 = RcT + 9 * c;
         const T t0 = T(tc[3 * c]), t1 = T(tc[3 * c + 1]), t2 = T(tc[3 * c + 2]);
         T acc[UST];
 #pragma unroll
@@ -976,12 +974,10 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
           continue;
         }
         const int ca = cslot[blk_a[blk]], cbb = cslot[blk_b[blk]];
-        T Ra[9], Rb[9];
-#pragma unroll
-        for (int i = 0; i < 9; ++i) {
-          Ra[i] = RcT[9 * ca + i];
-          Rb[i] = RcT[9 * cbb + i];
-        }
+        // rotations read from shared memory (uniform broadcast loads) rather
+        // than held in registers: keeps the fp64 job within the register budget
+        const T* Ra = RcT + 9 * ca;
+        const T* Rb = RcT + 9 * cbb;
         T acc[36];
 #pragma unroll
         for (int i = 0; i < 36; ++i) acc[i] = T(0);
