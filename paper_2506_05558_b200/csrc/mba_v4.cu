@@ -1451,6 +1451,10 @@ static int launch_t(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutp
   P.cfg = *cfg;
   P.o = *o;
   P.arena = smem - Fixed<T>::kBytes;
+  if (const char* e = getenv("MBA_V4_ARENA_CAP")) {   // tests: force the overflow re-solve path
+    const size_t cap = (size_t)atol(e);
+    if (cap < P.arena) P.arena = cap;
+  }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)d->n_problems * R);
   lc.blockDim = dim3(NT);

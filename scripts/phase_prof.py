@@ -14,7 +14,7 @@ sys.path[:0] = [REPO, os.path.join(REPO, "src")]
 os.environ["MBA_LIB"] = os.environ.get("MBA_PROF_LIB") or os.path.join(REPO, "paper_2506_05558_b200", "libminiba_prof.so")
 
 PHASES = ["setup", "cost0", "point", "jobs", "assemble", "cholesky", "solve+backsub", "trials", "commit",
-          "chol_panel_A", "chol_trailing_B"]
+          "ldl", "unused", "trial_sets", "try0"]
 
 
 def main():
@@ -35,7 +35,7 @@ def main():
     prm = solver.LmParams(max_iters=c["max_iters"], loss=c["loss"], precision=a.precision,
                           kernel=a.kernel)
     L = _lib.lib()
-    buf = torch.zeros(16, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(32, dtype=torch.int64, device="cuda")
     L.mba_debug_set_phase_buffer.argtypes = [ct.c_void_p]
     sol = solver.solve(db, prm)
     torch.cuda.synchronize()

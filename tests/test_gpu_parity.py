@@ -97,7 +97,7 @@ def test_deterministic_repeat(cuda_ok):
         np.testing.assert_array_equal(x["points"], y["points"])
 
 
-@pytest.mark.parametrize("kernel", ["cta", "grid"])
+@pytest.mark.parametrize("kernel", ["cta", "grid", "auto"])
 @pytest.mark.parametrize("precision", ["mixed", "f64"])
 def test_paper_scale_single_problem(precision, kernel, cuda_ok):
     """BASELINE config 2: 8 frames, K = 20k, Huber."""
@@ -186,3 +186,34 @@ def test_grid_mode_config5_shape(cuda_ok):
     ref = O.lm(p, max_iters=6, loss="cauchy")
     assert_parity(dev, ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"], p["R"], p["t"],
                   p["focal"], label="grid32")
+
+
+def test_cluster_kernel_plans(cuda_ok):
+    """The auto path takes the cluster-resident kernel: one CTA per config-4
+    problem, a 16 (f64) / 8 (mixed) CTA cluster for a config-2 problem."""
+    from paper_2506_05558_b200 import solver
+    from paper_2506_05558_b200.synth import make_batch
+    small = solver.to_device(solver.pack_synth(make_batch(4, n_cams=8, K=2000, seed=1)))
+    big = solver.to_device(solver.pack_synth(make_batch(1, n_cams=8, K=20000, seed=2)))
+    assert solver.plan(small, solver.LmParams(precision="f64")) == 1
+    assert solver.plan(small, solver.LmParams(precision="mixed")) == 1
+    assert solver.plan(big, solver.LmParams(precision="f64")) == 16
+    assert solver.plan(big, solver.LmParams(precision="mixed")) == 8
+
+
+def test_plan_overflow_is_resolved_by_cta_kernel(cuda_ok, monkeypatch):
+    """Problems whose slice does not fit the cluster kernel's shared-memory
+    plan are flagged and re-solved by the CTA kernel in the same mba_solve:
+    results match the oracle either way."""
+    from paper_2506_05558_b200.synth import make_batch
+    b = make_batch(6, n_cams=8, K=2000, seed=11)
+    probs = [b.problem(i) for i in range(6)]
+    normal = run_device(probs, dict(max_iters=200), "f64", "auto")
+    monkeypatch.setenv("MBA_V4_ARENA_CAP", "20000")   # every problem overflows
+    forced = run_device(probs, dict(max_iters=200), "f64", "auto")
+    for i in (0, 3):
+        ref = O.lm(probs[i], max_iters=200)
+        for dev in (normal[i], forced[i]):
+            assert dev["status"] in (1, 2)
+            assert_parity(dev, ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"],
+                          probs[i]["R"], probs[i]["t"], probs[i]["focal"], label=f"overflow[{i}]")
