@@ -248,9 +248,19 @@ def main():
     from paper_2506_05558_b200 import dist as mdist
     from paper_2506_05558_b200 import solver
 
-    torch.cuda.set_device(local)
+    # MBA_BENCH_ONE_GPU=1 (tests only): every rank on GPU 0 and the (tiny)
+    # collectives over gloo on host copies -- exercises the N-rank flow on a
+    # one-GPU box; production runs use NCCL with one rank per GPU.
+    one_gpu = os.environ.get("MBA_BENCH_ONE_GPU") == "1"
+    dev_index = 0 if one_gpu else local
+    torch.cuda.set_device(dev_index)
+    backend = "gloo" if one_gpu else "nccl"
+    coll = "cpu" if one_gpu else "cuda"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = c["n_problems"]
     lo, hi = mdist.shard_range(B, rank, world)
     t_gen = time.perf_counter()
@@ -268,7 +278,7 @@ def main():
     cfg_json["l2"] = ("inputs larger than L2 (%.2f GB per rank)" % (in_bytes / 1e9) if flush is None
                       else "L2 flushed (256 MB write) between timed steps")
     rows = mdist.padded_rows(B, world)
-    gbufs = [torch.empty((rows, mdist.SUMMARY_WIDTH), dtype=torch.float64, device="cuda")
+    gbufs = [torch.empty((rows, mdist.SUMMARY_WIDTH), dtype=torch.float64, device=coll)
              for _ in range(world)]
 
     def gather_step():
@@ -276,7 +286,13 @@ def main():
         if world == 1:
             return None
         local = mdist.pack_summary(torch, sol.final_stats, sol.n_iters, sol.status, rows, "cuda")
-        return mdist.gather_summaries(torch, dist, local, B, world, gbufs)
+        return mdist.gather_summaries(torch, dist, local.to(coll), B, world, gbufs)
+
+    def all_reduce(x, op):
+        if world > 1:
+            y = x.to(coll)
+            dist.all_reduce(y, op=op)
+            x.copy_(y)
 
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -290,7 +306,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         for i in range(args.steps):
             if flush is not None:
                 flush.fill_(i & 0xFF)
@@ -303,16 +319,14 @@ def main():
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    all_reduce(tot, dist.ReduceOp.MAX)
     total_ms = float(tot.item())
 
     n_iters = sol.n_iters.cpu().numpy()
     evals = sol.evals.cpu().numpy()
     status = sol.status.cpu().numpy()
     it_tot = torch.tensor([float(n_iters.sum())], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(it_tot)
+    all_reduce(it_tot, dist.ReduceOp.SUM)
     value = B * args.steps / (total_ms / 1e3)
     iters_per_s = float(it_tot.item()) * args.steps / (total_ms / 1e3)
 
@@ -356,8 +370,7 @@ def main():
         e_e.record(ps.copy)
         torch.cuda.synchronize()
         e_ms = torch.tensor([e_s.elapsed_time(e_e)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        all_reduce(e_ms, dist.ReduceOp.MAX)
         e2e = {"value": B * args.steps / (float(e_ms.item()) / 1e3), "unit": "problems/s",
                "h2d_bytes_per_step": int(ps.h2d_bytes), "d2h_bytes_per_step": int(ps.d2h_bytes),
                "ms_per_step": float(e_ms.item()) / args.steps, "chunks": len(ps.parts),
