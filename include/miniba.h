@@ -133,6 +133,11 @@ int32_t mba_solve(const MbaBatchDesc* desc, const MbaLmConfig* cfg, const MbaOut
  * per problem, -3 point-wise, -4 whole-GPU cooperative; 0 = not solvable. */
 int32_t mba_solve_plan(const MbaBatchDesc* desc, const MbaLmConfig* cfg);
 
+/* Number of kernel launches one mba_solve call issues for this batch and config
+ * (the cluster-resident kernel plus, when some problem may exceed its plan, the
+ * CTA kernel restricted to those problems). */
+int32_t mba_solve_launches(const MbaBatchDesc* desc, const MbaLmConfig* cfg);
+
 /* ---- stage entry points (float64), for the reference's internal API ---- */
 
 /* BaProblem.residuals (miniba.py:85-98): r [K][2], p_cam [K][3], bad [K] */

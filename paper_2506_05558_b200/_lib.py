@@ -60,6 +60,8 @@ def lib():
     L.mba_solve.restype = i32
     L.mba_solve_plan.restype = i32
     L.mba_solve_plan.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig)]
+    L.mba_solve_launches.restype = i32
+    L.mba_solve_launches.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig)]
     L.mba_solve.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig),
                             ct.POINTER(MbaOutputs), _vp, sz, _vp]
     L.mba_residuals.restype = i32
@@ -84,7 +86,7 @@ def lib():
     return L
 
 
-EXPORTED = ("mba_abi_version", "mba_workspace_bytes", "mba_solve", "mba_solve_plan", "mba_residuals", "mba_robust",
+EXPORTED = ("mba_abi_version", "mba_workspace_bytes", "mba_solve", "mba_solve_plan", "mba_solve_launches", "mba_residuals", "mba_robust",
             "mba_blocks", "mba_assemble", "mba_solve_step_scratch_bytes", "mba_solve_step",
             "mba_pose_lm")
 

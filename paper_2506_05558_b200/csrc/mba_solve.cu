@@ -2389,7 +2389,7 @@ static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutput
     const int R = v4::plan_cluster(d, cfg);
     if (R > 0) {
       int rc = v4::launch(d, cfg, o, st, R);
-      if (rc != MBA_OK) return rc;
+      if (rc != MBA_OK || !v4::may_overflow(d, cfg)) return rc;
       return launch_cfg<T, 8, false>(d, cfg, o, ws, ws_bytes, st, 1);
     }
     if (mode == 9) return MBA_ERR_TOO_LARGE;
@@ -2458,6 +2458,13 @@ int32_t mba_solve_plan(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
     mode = 2;
   }
   return -mode;
+}
+
+int32_t mba_solve_launches(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
+  const int32_t p = mba_solve_plan(d, cfg);
+  if (p == 0) return 0;
+  if (p > 0) return mba::v4::may_overflow(d, cfg) ? 2 : 1;
+  return 1;
 }
 
 int32_t mba_solve(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o,

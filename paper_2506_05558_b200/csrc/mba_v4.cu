@@ -1505,6 +1505,26 @@ static int launch_prec(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaO
   }
 }
 
+// Exact shared-memory need of the largest problem on a one-CTA plan (the
+// descriptor maxima bound every problem's slice): when it fits, no problem can
+// overflow and the re-solve launch is skipped.
+template <typename T>
+static bool may_overflow_t(const MbaBatchDesc* d, const Plan& p) {
+  if (p.R != 1 || getenv("MBA_V4_ARENA_CAP")) return true;
+  const size_t nlo = (size_t)d->max_obs, nlp = (size_t)d->max_points;
+  const size_t need = al16(16 * nlo) + al16(24 * nlp) + al16(sizeof(T) * jstr<T>() * nlo) +
+                      al16(sizeof(T) * PSTR * nlp) + al16(4 * nlp) + al16(2 * nlo) + al16(2 * (nlp + 1)) +
+                      4 * (size_t)d->max_pairs;
+  const size_t arena = smem_per_cta(p.per_sm, 256) - Fixed<T>::kBytes;
+  return nlo >= 65535 || need > arena;
+}
+
+int may_overflow(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
+  const Plan p = plan(d, cfg);
+  if (p.R == 0) return 1;
+  return cfg->precision == MBA_LIN_F64 ? may_overflow_t<double>(d, p) : may_overflow_t<float>(d, p);
+}
+
 int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st, int R) {
   Plan p = plan(d, cfg);
   if (p.R != R || R == 0) return MBA_ERR_TOO_LARGE;

@@ -19,11 +19,15 @@ constexpr int kStatusPlanOverflow = -2;
 // outside its envelope (more than 8 cameras, too large for a 16-CTA cluster).
 int plan_cluster(const MbaBatchDesc* d, const MbaLmConfig* cfg);
 
-// Launch the solver; returns MBA_OK / negative MbaStatus. *any_overflow is set
-// to 1 when some problem may report kStatusPlanOverflow (the caller then runs
-// the fallback kernel restricted to those problems).
+// Launch the solver; returns MBA_OK / negative MbaStatus. Problems that do not
+// fit report kStatusPlanOverflow (the caller then runs the CTA kernel
+// restricted to those problems).
 int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st,
            int cluster);
+
+// 0 when no problem of the batch can exceed the plan (one CTA per problem and
+// the descriptor maxima fit), so the overflow re-solve launch can be skipped.
+int may_overflow(const MbaBatchDesc* d, const MbaLmConfig* cfg);
 
 #ifdef MBA_PHASE_PROF
 void set_prof(unsigned long long* p);

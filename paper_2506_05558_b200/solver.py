@@ -285,15 +285,26 @@ def solve(db: DeviceBatch, prm: LmParams, sol: Solution | None = None) -> Soluti
     return sol
 
 
-def plan(db: DeviceBatch, prm: LmParams) -> int:
-    """Device path mba_solve takes (mba_solve_plan): cluster size R > 0 of the
-    cluster-resident kernel, or -1 warp / -2 CTA / -3 point-wise / -4 grid."""
+def _desc(db, prm):
     sol = Solution.__new__(Solution)
     for k in ("R", "t", "focal", "points", "costs", "lambdas", "accepted", "evals", "n_iters", "status",
               "final_stats"):
         setattr(sol, k, None)
     d, c, _ = descriptors(db, prm, sol)
+    return d, c
+
+
+def plan(db: DeviceBatch, prm: LmParams) -> int:
+    """Device path mba_solve takes (mba_solve_plan): cluster size R > 0 of the
+    cluster-resident kernel, or -1 warp / -2 CTA / -3 point-wise / -4 grid."""
+    d, c = _desc(db, prm)
     return int(_lib.lib().mba_solve_plan(ct.byref(d), ct.byref(c)))
+
+
+def launches(db: DeviceBatch, prm: LmParams) -> int:
+    """Kernel launches per mba_solve call (mba_solve_launches)."""
+    d, c = _desc(db, prm)
+    return int(_lib.lib().mba_solve_launches(ct.byref(d), ct.byref(c)))
 
 
 def fetch(sol: Solution, b: int = 0) -> dict:
@@ -345,8 +356,10 @@ class PipelinedSolver:
         self.prm = prm
         self.parts, self.cuts = split_host_batch(hb, n_chunks)
         self.pinned = [pin(p) for p in self.parts]
-        self.copy = torch.cuda.Stream()
+        self.copy = torch.cuda.Stream()      # host -> device
         self.compute = torch.cuda.Stream()
+        self.back = torch.cuda.Stream()      # device -> host (own stream: a chunk's read-back
+        #                                      must not hold up the next chunk's upload)
         self.dev = [to_device(p, pinned=self.pinned[i]) for i, p in enumerate(self.parts)]
         torch.cuda.synchronize()
         self.sols = [Solution(d, prm.max_iters) for d in self.dev]
@@ -371,8 +384,19 @@ class PipelinedSolver:
                 solve(d, self.prm, self.sols[i])
                 done = torch.cuda.Event()
                 done.record(self.compute)
-            self.copy.wait_event(done)
-            with torch.cuda.stream(self.copy):
+            self.back.wait_event(done)
+            with torch.cuda.stream(self.back):
                 for k in self.OUT:
                     self.host[i][k].copy_(getattr(self.sols[i], k), non_blocking=True)
+        # the next run's uploads overwrite the device inputs and its solves the
+        # device outputs: order them after this run's solves and read-backs
+        self.copy.wait_stream(self.compute)
+        self.copy.wait_stream(self.back)
         return self
+
+    def wait(self):
+        """Make the current stream wait for every copy and solve of run()."""
+        torch = _lib.torch_cuda()
+        cur = torch.cuda.current_stream()
+        for s_ in (self.copy, self.compute, self.back):
+            cur.wait_stream(s_)
