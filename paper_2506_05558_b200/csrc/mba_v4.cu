@@ -50,11 +50,13 @@ namespace cg = cooperative_groups;
 namespace mba {
 namespace v4 {
 
-constexpr int NW_MAX = 16;                       // layout bound: warps per CTA
-#ifndef MBA_NWF_LDL
-#define MBA_NWF_LDL 2
+#ifndef MBA_COST_U
+#define MBA_COST_U 4
 #endif
-constexpr int NWF_LDL = MBA_NWF_LDL;   // warps in the reduced-system factorisation
+#ifndef MBA_COST4_U
+#define MBA_COST4_U 2
+#endif
+constexpr int NW_MAX = 16;                       // layout bound: warps per CTA
 constexpr int MAXN = 8;                          // cameras per problem
 constexpr int MAXC = 6 * MAXN + 1;               // reduced system size (+ focal)
 constexpr int MAXNB = MAXN * (MAXN + 1) / 2;     // camera blocks a <= b
@@ -406,7 +408,6 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   T* l10s = (T*)(smem + F::oL10);
 
   __shared__ int s_flag, s_nf, s_nlp, s_npairs, s_job;
-  __shared__ int s_cf[2];   // pivot failure flags
   __shared__ unsigned char s_jorder[MAXN + MAXNB];   // job queue order: longest first
   __shared__ int s_wtot[NW_MAX];
   int epoch = 0;
@@ -475,11 +476,19 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   bool overflow = al16(16 * (size_t)nlo) + nlo > P.arena || nlo >= 65535;
   if (tid == 0 && k1 < k0) s_flag = 1;
   if (!overflow) {
-    for (int kl = tid; kl < nlo; kl += NT) {
-      const float4 rec = __ldg(reinterpret_cast<const float4*>(gobs) + k0 + kl);
-      const int c = __float_as_int(rec.z), pt = __float_as_int(rec.w);
-      if (pt < 0 || pt >= Pn || c < 0 || c >= n) s_flag = 1;
-      sobs[kl] = rec;
+    // eight 16-byte loads in flight per thread (one HBM round trip per 2k records)
+    for (int k8 = tid; k8 < nlo; k8 += 8 * NT) {
+      float4 rec[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k8 + u * NT < nlo) rec[u] = __ldg(reinterpret_cast<const float4*>(gobs) + k0 + k8 + u * NT);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (k8 + u * NT >= nlo) continue;
+        const int c = __float_as_int(rec[u].z), pt = __float_as_int(rec[u].w);
+        if (pt < 0 || pt >= Pn || c < 0 || c >= n) s_flag = 1;
+        sobs[k8 + u * NT] = rec[u];
+      }
     }
     __syncthreads();
     int cnt = 0;
@@ -561,7 +570,17 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     }
     if (tid == 0) ptr[nlp] = (unsigned short)nlo;
     __syncthreads();
-    for (int i = tid; i < nlp * 3; i += NT) Xs[i] = O.points_in[(pb + lpt[i / 3]) * 3 + i % 3];
+    for (int i8 = tid; i8 < nlp * 3; i8 += 8 * NT) {   // gathered point loads, eight in flight
+      double xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i8 + u * NT;
+        if (i < nlp * 3) xv[u] = __ldg(O.points_in + (pb + lpt[i / 3]) * 3 + i % 3);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i8 + u * NT < nlp * 3) Xs[i8 + u * NT] = xv[u];
+    }
     // camera-major permutation of the slice (warp per camera, ballot sweeps)
     for (int c = wid; c < n; c += NW) {
       int cnt = 0;
@@ -611,34 +630,57 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         const int ca = cslot[blk_a[blk]], cbb = cslot[blk_b[blk]];
         const int q1 = cam_ptr[ca + 1];
         int basep = pass ? blk_off[blk] : 0;
-        for (int q0 = cam_ptr[ca]; q0 < q1; q0 += 32) {
-          const int q = q0 + lane;
-          int i = -1, j0 = 0, j1 = 0, m = 0;
-          unsigned nib = 0u;
-          if (q < q1) {
-            i = perm[q];
-            const int sl = __float_as_int(sobs[i].w);
-            j0 = ptr[sl];
-            j1 = ptr[sl + 1];
+        const unsigned lt = (1u << lane) - 1u;
+        // two 32-observation chunks per step (their loads overlap); 0/1
+        // multiplicities -- one observation per (camera, point), the usual
+        // case -- are counted / compacted with ballots
+        for (int q0 = cam_ptr[ca]; q0 < q1; q0 += 64) {
+          int i[2], j0[2], m[2];
+          unsigned nib[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int q = q0 + 32 * u + lane;
+            i[u] = -1;
+            j0[u] = 0;
+            nib[u] = 0u;
+            if (q < q1) {
+              i[u] = perm[q];
+              const int sl = __float_as_int(sobs[i[u]].w);
+              j0[u] = ptr[sl];
+              nib[u] = (cpos[sl] >> (4 * cbb)) & 15u;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
             // self pairs (j == i) are folded into the camera jobs
-            nib = (cpos[sl] >> (4 * cbb)) & 15u;
-            if (nib == 15u) {
-              for (int j = j0; j < j1; ++j) m += __float_as_int(sobs[j].z) == cbb && j != i;
+            m[u] = 0;
+            if (nib[u] == 15u) {
+              const int j1 = ptr[__float_as_int(sobs[i[u]].w) + 1];
+              for (int j = j0[u]; j < j1; ++j) m[u] += __float_as_int(sobs[j].z) == cbb && j != i[u];
             } else {
-              m = nib != 0u && j0 + (int)nib - 1 != i;
+              m[u] = (nib[u] != 0u && j0[u] + (int)nib[u] - 1 != i[u]) ? 1 : 0;
             }
-          }
-          if (pass) {
-            const int inc = warp_incl_scan(m, lane);
-            int pos = basep + inc - m;
-            if (nib == 15u) {
-              for (int j = j0; j < j1 && m; ++j)
-                if (__float_as_int(sobs[j].z) == cbb && j != i) pairs[pos++] = ((unsigned)i << 16) | (unsigned)j;
-            } else if (m) {
-              pairs[pos] = ((unsigned)i << 16) | (unsigned)(j0 + (int)nib - 1);
+            int excl, cnt;
+            if (!__any_sync(0xffffffffu, nib[u] == 15u)) {
+              const unsigned bal = __ballot_sync(0xffffffffu, m[u] != 0);
+              excl = __popc(bal & lt);
+              cnt = __popc(bal);
+            } else {
+              excl = warp_incl_scan(m[u], lane) - m[u];
+              cnt = warp_sum(m[u]);
             }
+            if (pass && m[u]) {
+              int pos = basep + excl;
+              if (nib[u] == 15u) {
+                const int j1 = ptr[__float_as_int(sobs[i[u]].w) + 1];
+                for (int j = j0[u]; j < j1; ++j)
+                  if (__float_as_int(sobs[j].z) == cbb && j != i[u]) pairs[pos++] = ((unsigned)i[u] << 16) | (unsigned)j;
+              } else {
+                pairs[pos] = ((unsigned)i[u] << 16) | (unsigned)(j0[u] + (int)nib[u] - 1);
+              }
+            }
+            basep += cnt;
           }
-          basep += warp_sum(m);
         }
         if (!pass && lane == 0) blk_off[blk + 1] = basep;
       }
@@ -705,7 +747,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
                   double out[3]) {
     constexpr bool FULL = decltype(full)::value;
     double acc[3] = {0.0, 0.0, 0.0};
-    constexpr int U = 4;
+    constexpr int U = MBA_COST_U;
     for (int c0 = tid; c0 < nlo; c0 += U * NT) {
       float4 o[U];
 #pragma unroll
@@ -754,7 +796,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   // four rank-ordered sums (identical to four separate passes)
   auto cost4 = [&](const double (&fts)[4], double (&out)[4]) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    constexpr int U = 2;
+    constexpr int U = MBA_COST4_U;
     for (int c0 = tid; c0 < nlo; c0 += U * NT) {
       float4 o[U];
 #pragma unroll

@@ -14,7 +14,8 @@ sys.path[:0] = [REPO, os.path.join(REPO, "src")]
 os.environ["MBA_LIB"] = os.environ.get("MBA_PROF_LIB") or os.path.join(REPO, "paper_2506_05558_b200", "libminiba_prof.so")
 
 PHASES = ["setup", "cost0", "point", "jobs", "assemble", "cholesky", "solve+backsub", "trials", "commit",
-          "ldl", "unused", "trial_sets", "try0"]
+          "ldl", "unused", "setup_stage_validate", "setup_slots_X", "setup_perm", "setup_pairs",
+          "setup_jobs_tab"]
 
 
 def main():
