@@ -438,6 +438,56 @@ __global__ void bench_r2b(const T* __restrict__ Ain, int C, int reps, long long*
   for (int i = tid; i < CA; i += NT) out[i] = S[i];
 }
 
+
+// wavefront (fan-in, column-cyclic): warp w owns columns j = w (mod 8); for
+// each own column it applies the updates of columns k < j as soon as their
+// ready flags are published, then publishes its own pivot. No CTA barrier.
+template <typename T>
+__global__ void bench_wave(const T* __restrict__ Ain, int C, int reps, long long* cyc, T* out) {
+  __shared__ T S[MAXCA], S0[MAXCA], invd[64];
+  __shared__ volatile int ready[64];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NWW = NT / 32;
+  const int CA = C * (C + 3) / 2;
+  for (int i = tid; i < CA; i += NT) S0[i] = Ain[i];
+  __syncthreads();
+  long long tot = 0;
+  for (int r = 0; r < reps; ++r) {
+    for (int i = tid; i < CA; i += NT) S[i] = S0[i];
+    if (tid < 64) ready[tid] = 0;
+    __syncthreads();
+    long long t0 = clock64();
+    const int epoch = r + 1;
+    for (int j = wid; j < C; j += NWW) {
+      T* colj = S + acol(j, C) - j;   // colj[i] = S[i][j], i in [j, C]
+      const int i0 = j + lane, i1 = j + lane + 32;
+      T x0 = i0 <= C ? colj[i0] : T(0);
+      T x1 = i1 <= C ? colj[i1] : T(0);
+      for (int k = 0; k < j; ++k) {
+        const T* colk = S + acol(k, C) - k;
+        if (lane == 0) while (ready[k] != epoch) { }
+        __syncwarp();
+        __threadfence_block();
+        const T l = colk[j] * invd[k];            // L_jk
+        if (i0 <= C) x0 -= colk[i0] * l;
+        if (i1 <= C) x1 -= colk[i1] * l;
+      }
+      const T d = __shfl_sync(0xffffffffu, x0, 0);   // row j = lane 0
+      const T inv = frcp(d);
+      if (i0 <= C) colj[i0] = x0;
+      if (i1 <= C) colj[i1] = x1;
+      if (lane == 0) invd[j] = inv;
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) ready[j] = epoch;
+    }
+    __syncthreads();
+    tot += clock64() - t0;
+  }
+  if (tid == 0) cyc[0] = tot / reps;
+  for (int i = tid; i < CA; i += NT) out[i] = S[i];
+}
+
 template <typename T>
 void run(int C) {
   const int CA = C * (C + 3) / 2;
@@ -452,7 +502,7 @@ void run(int C) {
   cudaMalloc(&dA, CA * sizeof(T)); cudaMalloc(&dO, CA * sizeof(T)); cudaMalloc(&dc, 8);
   cudaMemcpy(dA, h.data(), CA * sizeof(T), cudaMemcpyHostToDevice);
   std::vector<T> ref(CA), o(CA);
-  const char* names[] = {"all-threads x4", "1 warp x4", "1 warp lane=row", "all-threads rank-2", "barrier only", "lds-sts-bar", "register-owned", "warp registers CM=43", "warp registers CM=49", "rank-2 fast-rcp regs", "rank-1 fast-rcp regs", "rank-2 1-barrier"};
+  const char* names[] = {"all-threads x4", "1 warp x4", "1 warp lane=row", "all-threads rank-2", "barrier only", "lds-sts-bar", "register-owned", "warp registers CM=43", "warp registers CM=49", "rank-2 fast-rcp regs", "rank-1 fast-rcp regs", "rank-2 1-barrier", "wavefront flags"};
   auto go = [&](auto kern, int v) {
     kern<<<1, NT>>>(dA, C, 50, dc, dO);
     long long c; cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
@@ -461,7 +511,7 @@ void run(int C) {
     double err = 0; for (int i = 0; i < CA; ++i) err = fmax(err, fabs((double)o[i] - (double)ref[i]) / (1e-30 + fabs((double)ref[i])));
     printf("%s C=%d %-20s %6lld cycles  maxrel %.2e  %s\n", sizeof(T) == 4 ? "f32" : "f64", C, names[v], c, err, cudaGetErrorString(cudaGetLastError()));
   };
-  go(bench<T, 0>, 0); go(bench<T, 3>, 3); go(bench_r2f<T>, 9); go(bench_r2b<T>, 11);
+  go(bench<T, 0>, 0); go(bench<T, 3>, 3); go(bench_r2b<T>, 11); go(bench_wave<T>, 12);
 }
 
 int main() {

@@ -241,3 +241,29 @@ def test_pipelined_host_to_host_solver_matches_device_solve(cuda_ok):
         np.testing.assert_array_equal(h["n_iters"].numpy(), sol.n_iters[a:z].cpu().numpy())
         p0, p1 = hb.pt_off[a], hb.pt_off[z]
         np.testing.assert_array_equal(h["points"].numpy(), sol.points[p0:p1].cpu().numpy())
+
+
+def test_heterogeneous_batch_cluster_kernel(cuda_ok):
+    """One batch mixing camera counts (3..8), sizes (K 300..3000), free /
+    fixed focal, fixed points and two fixed cameras: every problem matches the
+    oracle under the parity rule (the cluster kernel plans for the batch maxima
+    and handles each problem's own layout)."""
+    from paper_2506_05558_b200.synth import make_batch
+    probs = []
+    specs = [(3, 300, True, True), (8, 3000, True, True), (5, 1200, False, True), (8, 2000, True, False),
+             (6, 800, True, True), (4, 600, False, False), (8, 2400, True, True)]
+    for s, (n, K, of, op) in enumerate(specs):
+        p = make_batch(1, n_cams=n, K=K, seed=100 + s).problem(0)
+        p["optimize_focal"] = of
+        p["optimize_points"] = op
+        if s == 6:
+            p["fixed_cams"] = np.array([True, True] + [False] * (n - 2))
+        probs.append(p)
+    devs = run_device(probs, dict(max_iters=100), "f64", "auto")
+    for i, (p, dev) in enumerate(zip(probs, devs)):
+        q = dict(p)                      # the oracle rebinds q's R, t, focal, points
+        ref = O.lm(q, max_iters=100)
+        assert_parity(dev, ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"], q["R"], q["t"],
+                      q["focal"], label=f"hetero[{i}]")
+        if not p["optimize_points"]:
+            np.testing.assert_array_equal(dev["points"], p["points"])
