@@ -188,6 +188,19 @@ int32_t mba_pose_lm(int32_t nb, int32_t m, const double* X, const double* uv, do
                     const double* X_all, const double* uv_all, double inlier_px,
                     int32_t* inliers, double* inlier_sse, void* stream);
 
+/* Batched triangulation (triangulate, miniba.py:458-530), one
+ * track per thread: track k's observations are [obs_off[k], obs_off[k+1]) with
+ * camera index cam[] into R [n_cams][3][3] / t [n_cams][3] and pixel uv[][2].
+ * Widest-angle ray pair midpoint, gn_steps Gauss-Newton steps, mean
+ * reprojection check. Outputs X [n_tracks][3] (NaN on failure), status
+ * [n_tracks] (0 ok, 1 fewer than two views, 2 baseline angle <= min_angle_deg,
+ * 3 parallel rays, 4 point behind a camera, 5 mean reprojection > max_reproj_px
+ * -- the reference's TriangulationFailure cases), mean_err [n_tracks] (may be NULL). */
+int32_t mba_triangulate(int32_t n_tracks, const int64_t* obs_off, const int32_t* cam, const double* uv,
+                        int32_t n_cams, const double* R, const double* t, double focal, double cx,
+                        double cy, double max_reproj_px, double min_angle_deg, int32_t gn_steps,
+                        double* X, int32_t* status, double* mean_err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

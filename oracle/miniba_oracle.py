@@ -17,6 +17,7 @@ are `miniba.py:<line>` relative to `/root/reference/pkg/src/gsrecon/`):
 * damped Schur / dense solve      -> `damped_step`     (miniba.py:180-220)
 * LM loop with 5-try backtracking -> `lm`              (miniba.py:223-296)
 * batched pose-only LM            -> `pose_lm`         (miniba.py:303-389)
+* triangulation of one track      -> `triangulate`     (miniba.py:458-530)
 
 Extensions that the reference does NOT have (documented in DESIGN.md):
 
@@ -368,6 +369,68 @@ def pose_lm(R0, t0, X, uv, f, cx, cy, iters, lambda_init=1e-5, nu=2.0, delta=2.0
         lam = np.where(better, np.maximum(lam / nu, 1e-15), np.minimum(lam * nu, LAMBDA_MAX))
         cost, aux = _pose_eval(R, t, X, uv, f, cx, cy, delta)
     return R, t, cost
+
+
+# ----------------------------------------------------------------------------
+# triangulation (miniba.py:458-530), status codes instead of exceptions
+
+TRI_OK, TRI_FEW, TRI_BASELINE, TRI_PARALLEL, TRI_BEHIND, TRI_REPROJ = range(6)
+
+
+def triangulate(Rs, ts, px, f, cx, cy, max_reproj_px=8.0, min_angle_deg=0.5, gn_steps=3):
+    """One track: rays of every view (camera centre -R^T t, direction R^T K^-1 uv,
+    normalised), the pair with the widest angle (first in (i, j) order on ties),
+    the midpoint of its closest points, then `gn_steps` Gauss-Newton steps on
+    the reprojection error with H = J^T J + 1e-12 I. Returns (X, status)."""
+    n = len(Rs)
+    if n < 2:
+        return np.full(3, np.nan), TRI_FEW
+    px = np.asarray(px, np.float64)
+    origins = np.stack([-R.T @ t for R, t in zip(Rs, ts)])
+    dirs = np.empty((n, 3))
+    for i in range(n):
+        d = Rs[i].T @ np.array([(px[i, 0] - cx) / f, (px[i, 1] - cy) / f, 1.0])
+        dirs[i] = d / np.linalg.norm(d)
+    best = (-1.0, 0, 1)
+    for i in range(n):
+        for j in range(i + 1, n):
+            ang = np.degrees(np.arccos(np.clip(np.abs(dirs[i] @ dirs[j]), -1, 1)))
+            if ang > best[0]:
+                best = (ang, i, j)
+    ang, i, j = best
+    if ang <= min_angle_deg:
+        return np.full(3, np.nan), TRI_BASELINE
+    d1, d2, o1, o2 = dirs[i], dirs[j], origins[i], origins[j]
+    a, b, c = d1 @ d1, d1 @ d2, d2 @ d2
+    rhs = o2 - o1
+    den = a * c - b * b
+    if den < 1e-18:
+        return np.full(3, np.nan), TRI_PARALLEL
+    s_ = (c * (d1 @ rhs) - b * (d2 @ rhs)) / den
+    u_ = (b * (d1 @ rhs) - a * (d2 @ rhs)) / den
+    X = 0.5 * (o1 + s_ * d1 + o2 + u_ * d2)
+    for _ in range(gn_steps):
+        J = np.zeros((2 * n, 3))
+        r = np.zeros(2 * n)
+        for k in range(n):
+            pc = Rs[k] @ X + ts[k]
+            if pc[2] <= 1e-12:
+                return np.full(3, np.nan), TRI_BEHIND
+            z = pc[2]
+            Jp = np.array([[f / z, 0, -f * pc[0] / z ** 2], [0, f / z, -f * pc[1] / z ** 2]])
+            J[2 * k:2 * k + 2] = Jp @ Rs[k]
+            r[2 * k] = f * pc[0] / z + cx - px[k, 0]
+            r[2 * k + 1] = f * pc[1] / z + cy - px[k, 1]
+        X = X - np.linalg.solve(J.T @ J + 1e-12 * np.eye(3), J.T @ r)
+    errs = np.empty(n)
+    for k in range(n):
+        pc = Rs[k] @ X + ts[k]
+        if pc[2] <= 1e-12:
+            return np.full(3, np.nan), TRI_BEHIND
+        errs[k] = np.hypot(f * pc[0] / pc[2] + cx - px[k, 0], f * pc[1] / pc[2] + cy - px[k, 1])
+    if errs.mean() > max_reproj_px:
+        return np.full(3, np.nan), TRI_REPROJ
+    return X, TRI_OK
 
 
 # ----------------------------------------------------------------------------

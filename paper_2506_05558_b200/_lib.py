@@ -60,6 +60,8 @@ def lib():
     L.mba_solve.restype = i32
     L.mba_solve_plan.restype = i32
     L.mba_solve_plan.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig)]
+    L.mba_triangulate.restype = i32
+    L.mba_triangulate.argtypes = [i32, _vp, _vp, _vp, i32, _vp, _vp, d, d, d, d, d, i32, _vp, _vp, _vp, _vp]
     L.mba_solve_launches.restype = i32
     L.mba_solve_launches.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig)]
     L.mba_solve.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig),
@@ -88,7 +90,7 @@ def lib():
 
 EXPORTED = ("mba_abi_version", "mba_workspace_bytes", "mba_solve", "mba_solve_plan", "mba_solve_launches", "mba_residuals", "mba_robust",
             "mba_blocks", "mba_assemble", "mba_solve_step_scratch_bytes", "mba_solve_step",
-            "mba_pose_lm")
+            "mba_pose_lm", "mba_triangulate")
 
 
 def check(rc, what):

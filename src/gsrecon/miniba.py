@@ -515,6 +515,40 @@ def triangulate(poses: list, pixels: np.ndarray, intr: CameraIntrinsics, max_rep
     return X
 
 
+TRIANGULATION_FAILURES = {1: "need at least two observations", 2: "baseline angle too small",
+                          3: "parallel rays", 4: "point behind a camera", 5: "mean reprojection too large"}
+
+
+def triangulate_batch(R: np.ndarray, t: np.ndarray, cam: np.ndarray, pixels: np.ndarray,
+                      obs_off: np.ndarray, intr: CameraIntrinsics, max_reproj_px: float = 8.0,
+                      min_angle_deg: float = 0.5, gn_steps: int = 3):
+    """`triangulate` (miniba.py:458-530) for many tracks in one device call
+    (mba_triangulate, one thread per track). Track k observes camera cam[j]
+    (rows of R (n,3,3) / t (n,3)) at pixels[j] for j in [obs_off[k],
+    obs_off[k+1]). Returns (X (T,3), status (T,), mean_err (T,)): status 0 is a
+    triangulated point; otherwise X is NaN and the status names the reference's
+    TriangulationFailure (TRIANGULATION_FAILURES)."""
+    torch = _torch()
+    off = np.asarray(obs_off, np.int64)
+    T = len(off) - 1
+    if T <= 0:
+        return np.zeros((0, 3)), np.zeros(0, np.int32), np.zeros(0)
+    dR = _dev(np.asarray(R, np.float64).reshape(-1, 3, 3))
+    dt = _dev(np.asarray(t, np.float64).reshape(-1, 3))
+    dcam = _dev(np.asarray(cam, np.int32))
+    duv = _dev(np.asarray(pixels, np.float64).reshape(-1, 2))
+    doff = _dev(off)
+    X = _empty((T, 3), torch.float64)
+    st = _empty((T,), torch.int32)
+    err = _empty((T,), torch.float64)
+    _lib.check(_lib.lib().mba_triangulate(T, ptr(doff), ptr(dcam), ptr(duv), int(dR.shape[0]), ptr(dR), ptr(dt),
+                                          float(intr.focal), float(intr.cx), float(intr.cy),
+                                          float(max_reproj_px), float(min_angle_deg), int(gn_steps),
+                                          ptr(X), ptr(st), ptr(err), _lib.stream_ptr()),
+               "mba_triangulate")
+    return _host(X), _host(st), _host(err)
+
+
 def rebootstrap_check(centers: np.ndarray, window: int = 20, min_dist: float = 0.1 / 3.0) -> bool:
     """True when the mean consecutive camera-centre distance over the last
     `window` centres is below min_dist (miniba.py:861-873)."""

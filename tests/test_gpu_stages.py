@@ -119,3 +119,20 @@ def test_bootstrap_matches_reference(seed, cuda_ok):
         np.testing.assert_allclose(p.R, R, atol=1e-6)
         np.testing.assert_allclose(p.translation, t, atol=1e-6)
     np.testing.assert_allclose(info["mean_err"], float(z["out_mean_err"]), rtol=1e-6)
+
+
+def test_triangulate_batch_matches_reference(cuda_ok):
+    """mba_triangulate (one thread per track) against the unmodified
+    reference's triangulate on 600 tracks of 2..8 views, including tiny
+    baselines, outliers and points behind the cameras: identical
+    success/failure classification, points to 1e-10."""
+    from gsrecon import miniba as M
+    from gsrecon.scene import CameraIntrinsics
+    z = np.load(f"{GOLDEN}/triangulate.npz")
+    intr = CameraIntrinsics(float(z["focal"]), float(z["cx"]), float(z["cy"]), 640, 480)
+    X, st, err = M.triangulate_batch(z["R"], z["t"], z["cam"], z["uv"], z["obs_off"], intr)
+    np.testing.assert_array_equal(st, z["status"])
+    ok = st == 0
+    np.testing.assert_allclose(X[ok], z["X"][ok], rtol=0, atol=1e-10)
+    assert np.all(np.isnan(X[~ok]))
+    assert np.all(err[ok] <= 8.0)
