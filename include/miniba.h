@@ -201,6 +201,20 @@ int32_t mba_triangulate(int32_t n_tracks, const int64_t* obs_off, const int32_t*
                         double cy, double max_reproj_px, double min_angle_deg, int32_t gn_steps,
                         double* X, int32_t* status, double* mean_err, void* stream);
 
+/* Batched descriptor matching (frontend.match, frontend.py:220-250; the
+ * exhaustive pairwise matching of build_tracks, miniba.py:555-591; SURVEY
+ * 8(f)-3). desc: n_frames' 256-bit descriptors, 32 bytes each, frame f's rows
+ * [desc_off[f], desc_off[f+1]). pairs: n_pairs (frame_a, frame_b). row_off_a /
+ * row_off_b [n_pairs]: where pair p's per-row outputs start for the rows of
+ * frame_a / frame_b; max_rows >= the largest frame. Per row of frame_a:
+ * match_b (index in frame_b of the mutual ratio-tested nearest neighbour, or -1)
+ * and dist (its Hamming distance); nn_ab/ok_a/best_ab/nn_ba/ok_b are the
+ * per-direction scratch results (caller-sized like the row offsets). */
+int32_t mba_match_pairs(int32_t n_frames, const uint8_t* desc, const int64_t* desc_off, int32_t n_pairs,
+                        const int32_t* pairs, const int64_t* row_off_a, const int64_t* row_off_b,
+                        int64_t max_rows, double ratio_max, int32_t* nn_ab, uint8_t* ok_a, int32_t* best_ab,
+                        int32_t* nn_ba, uint8_t* ok_b, int32_t* match_b, int32_t* dist, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,6 +18,7 @@ are `miniba.py:<line>` relative to `/root/reference/pkg/src/gsrecon/`):
 * LM loop with 5-try backtracking -> `lm`              (miniba.py:223-296)
 * batched pose-only LM            -> `pose_lm`         (miniba.py:303-389)
 * triangulation of one track      -> `triangulate`     (miniba.py:458-530)
+* descriptor matching of a pair   -> `match`           (frontend.py:220-250)
 
 Extensions that the reference does NOT have (documented in DESIGN.md):
 
@@ -431,6 +432,37 @@ def triangulate(Rs, ts, px, f, cx, cy, max_reproj_px=8.0, min_angle_deg=0.5, gn_
     if errs.mean() > max_reproj_px:
         return np.full(3, np.nan), TRI_REPROJ
     return X, TRI_OK
+
+
+# ----------------------------------------------------------------------------
+# descriptor matching (frontend.py:210-250)
+
+_POPC8 = np.array([bin(i).count("1") for i in range(256)], dtype=np.uint8)
+
+
+def match(desc_a, desc_b, ratio_max=0.95, bits=256):
+    """Mutual nearest neighbours in Hamming distance over packed descriptors,
+    best / second-best ratio test (second via np.partition, duplicates
+    counted). Returns (idx_a, idx_b, scores) sorted by idx_a."""
+    if len(desc_a) == 0 or len(desc_b) == 0:
+        return np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0)
+    d = _POPC8[desc_a[:, None, :] ^ desc_b[None, :, :]].sum(axis=-1, dtype=np.int32)
+
+    def nn_ratio(dist):
+        nn = np.argmin(dist, axis=1)
+        best = dist[np.arange(len(dist)), nn]
+        if dist.shape[1] >= 2:
+            second = np.partition(dist, 1, axis=1)[:, 1].astype(np.float64)
+            ratio = np.where(second > 0, best / np.maximum(second, 1e-12), 1.0)
+            return nn, ratio < ratio_max
+        return nn, np.ones(len(dist), dtype=bool)
+
+    nn_ab, ok_a = nn_ratio(d)
+    nn_ba, ok_b = nn_ratio(d.T)
+    ia = np.arange(len(desc_a))
+    mutual = (nn_ba[nn_ab] == ia) & ok_a & ok_b[nn_ab]
+    idx_a, idx_b = ia[mutual], nn_ab[mutual]
+    return idx_a.astype(np.int64), idx_b.astype(np.int64), 1.0 - d[idx_a, idx_b] / float(bits)
 
 
 # ----------------------------------------------------------------------------

@@ -60,6 +60,9 @@ def lib():
     L.mba_solve.restype = i32
     L.mba_solve_plan.restype = i32
     L.mba_solve_plan.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig)]
+    L.mba_match_pairs.restype = i32
+    L.mba_match_pairs.argtypes = [i32, _vp, _vp, i32, _vp, _vp, _vp, i64, d, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                  _vp]
     L.mba_triangulate.restype = i32
     L.mba_triangulate.argtypes = [i32, _vp, _vp, _vp, i32, _vp, _vp, d, d, d, d, d, i32, _vp, _vp, _vp, _vp]
     L.mba_solve_launches.restype = i32
@@ -90,7 +93,7 @@ def lib():
 
 EXPORTED = ("mba_abi_version", "mba_workspace_bytes", "mba_solve", "mba_solve_plan", "mba_solve_launches", "mba_residuals", "mba_robust",
             "mba_blocks", "mba_assemble", "mba_solve_step_scratch_bytes", "mba_solve_step",
-            "mba_pose_lm", "mba_triangulate")
+            "mba_pose_lm", "mba_triangulate", "mba_match_pairs")
 
 
 def check(rc, what):

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libminiba.so")
 LIB_PROF = os.path.join(HERE, "libminiba_prof.so")
-SOURCES = ["mba_solve.cu", "mba_v4.cu", "mba_stages.cu", "mba_pose.cu", "mba_tri.cu"]
+SOURCES = ["mba_solve.cu", "mba_v4.cu", "mba_stages.cu", "mba_pose.cu", "mba_tri.cu", "mba_match.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -515,6 +515,45 @@ def triangulate(poses: list, pixels: np.ndarray, intr: CameraIntrinsics, max_rep
     return X
 
 
+def match_batch(descriptors: list, pairs, ratio_max: float = 0.95) -> list:
+    """`frontend.match` (frontend.py:220-250) for every (i, j) in `pairs` in
+    one device call (mba_match_pairs): mutual nearest neighbours in Hamming
+    distance over 256-bit packed descriptors with the best/second ratio test.
+    descriptors: per frame (N_f, 32) uint8. Returns [(idx_a, idx_b, scores)]
+    per pair, sorted by idx_a, identical to the reference's."""
+    torch = _torch()
+    pairs = np.asarray(pairs, np.int32).reshape(-1, 2)
+    if len(pairs) == 0:
+        return []
+    sizes = np.array([len(d) for d in descriptors], np.int64)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    desc = np.concatenate([np.asarray(d, np.uint8).reshape(-1, 32) for d in descriptors]) \
+        if off[-1] else np.zeros((1, 32), np.uint8)
+    na, nb = sizes[pairs[:, 0]], sizes[pairs[:, 1]]
+    row_a = np.concatenate([[0], np.cumsum(na)]).astype(np.int64)
+    row_b = np.concatenate([[0], np.cumsum(nb)]).astype(np.int64)
+    ra, rb = max(int(row_a[-1]), 1), max(int(row_b[-1]), 1)
+    i32 = lambda n: _empty((n,), torch.int32)
+    u8 = lambda n: _empty((n,), torch.uint8)
+    nn_ab, ok_a, best_ab, match_b, dist = i32(ra), u8(ra), i32(ra), i32(ra), i32(ra)
+    nn_ba, ok_b = i32(rb), u8(rb)
+    d_desc, d_off, d_pairs = _dev(desc), _dev(off), _dev(pairs)
+    d_ra, d_rb = _dev(row_a[:-1]), _dev(row_b[:-1])
+    _lib.check(_lib.lib().mba_match_pairs(len(descriptors), ptr(d_desc), ptr(d_off), len(pairs), ptr(d_pairs),
+                                          ptr(d_ra), ptr(d_rb), int(max(sizes.max(), 1)), float(ratio_max),
+                                          ptr(nn_ab), ptr(ok_a), ptr(best_ab), ptr(nn_ba), ptr(ok_b),
+                                          ptr(match_b), ptr(dist), _lib.stream_ptr()),
+               "mba_match_pairs")
+    mb, dd = _host(match_b), _host(dist)
+    out = []
+    for p in range(len(pairs)):
+        m = mb[row_a[p]:row_a[p + 1]]
+        ia = np.flatnonzero(m >= 0).astype(np.int64)
+        ib = m[ia].astype(np.int64)
+        out.append((ia, ib, 1.0 - dd[row_a[p]:row_a[p + 1]][ia] / 256.0))
+    return out
+
+
 TRIANGULATION_FAILURES = {1: "need at least two observations", 2: "baseline angle too small",
                           3: "parallel rays", 4: "point behind a camera", 5: "mean reprojection too large"}
 

@@ -136,3 +136,21 @@ def test_triangulate_batch_matches_reference(cuda_ok):
     np.testing.assert_allclose(X[ok], z["X"][ok], rtol=0, atol=1e-10)
     assert np.all(np.isnan(X[~ok]))
     assert np.all(err[ok] <= 8.0)
+
+
+def test_match_batch_matches_reference(cuda_ok):
+    """mba_match_pairs for all 28 frame pairs of 8 frames against the
+    unmodified reference's frontend.match on the same descriptors (planted
+    correspondences with flipped bits, distractors, exact duplicates that
+    exercise the ratio test): identical indices and scores."""
+    from gsrecon import miniba as M
+    z = np.load(f"{GOLDEN}/match.npz")
+    off = z["desc_off"]
+    descs = [z["desc"][off[f]:off[f + 1]] for f in range(len(off) - 1)]
+    res = M.match_batch(descs, z["pairs"])
+    po = z["pair_off"]
+    assert sum(len(r[0]) for r in res) == po[-1]
+    for p, (ia, ib, sc) in enumerate(res):
+        np.testing.assert_array_equal(ia, z["idx_a"][po[p]:po[p + 1]])
+        np.testing.assert_array_equal(ib, z["idx_b"][po[p]:po[p + 1]])
+        np.testing.assert_array_equal(sc, z["score"][po[p]:po[p + 1]])
