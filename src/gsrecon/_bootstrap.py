@@ -25,15 +25,52 @@ def _find(parent, x):
     return root
 
 
+def filter_matches_flow(kps_a, kps_b, idx_a, idx_b, k: int = 6, base_tol: float = 3.0,
+                        rel_tol: float = 0.5) -> np.ndarray:
+    """Keep matches whose displacement agrees with the median displacement of
+    their k nearest matched neighbours (frontend.py:188-207): deviation <=
+    max(base_tol, rel_tol * |median|). Returns a keep mask."""
+    from scipy.spatial import cKDTree
+    if len(idx_a) < k + 1:
+        return np.ones(len(idx_a), dtype=bool)
+    pa = np.asarray(kps_a)[idx_a]
+    disp = np.asarray(kps_b)[idx_b] - pa
+    _, nb = cKDTree(pa).query(pa, k=k + 1)
+    med = np.median(disp[nb[:, 1:]], axis=1)
+    dev = np.linalg.norm(disp - med, axis=1)
+    return dev <= np.maximum(base_tol, rel_tol * np.linalg.norm(med, axis=1))
+
+
+def build_tracks_device(features: list, n_obs_max: int | None = None) -> list:
+    """`build_tracks(features, default_matcher)` (miniba.py:555-602) with the
+    exhaustive pairwise descriptor matching of all frame pairs in ONE device
+    call (match_batch -> mba_match_pairs); the flow filter and the union-find
+    grouping run on the host."""
+    from .miniba import match_batch
+    n = len(features)
+    pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+    res = dict(zip(pairs, match_batch([f[1] for f in features], pairs)))
+
+    def matcher_from_batch(i, j):
+        ia, ib, sc = res[(i, j)]
+        keep = filter_matches_flow(features[i][0], features[j][0], ia, ib)
+        return ia[keep], ib[keep], sc[keep]
+    return _group_tracks(features, matcher_from_batch, n_obs_max)
+
+
 def build_tracks(features: list, matcher, n_obs_max: int | None = None) -> list:
     """Union-find over all pairwise matches; tracks with two keypoints in one
     frame are dropped; observations ordered by frame; optionally capped to the
     most recent n_obs_max. Sorted by (first frame, first keypoint)."""
+    return _group_tracks(features, lambda i, j: matcher(features[i], features[j]), n_obs_max)
+
+
+def _group_tracks(features: list, pair_matches, n_obs_max: int | None) -> list:
     parent: dict = {}
     n = len(features)
     for i in range(n):
         for j in range(i + 1, n):
-            ia, ib, _ = matcher(features[i], features[j])
+            ia, ib, _ = pair_matches(i, j)
             for a, b in zip(ia, ib):
                 ra, rb = _find(parent, (i, int(a))), _find(parent, (j, int(b)))
                 if ra != rb:

@@ -154,3 +154,16 @@ def test_match_batch_matches_reference(cuda_ok):
         np.testing.assert_array_equal(ia, z["idx_a"][po[p]:po[p + 1]])
         np.testing.assert_array_equal(ib, z["idx_b"][po[p]:po[p + 1]])
         np.testing.assert_array_equal(sc, z["score"][po[p]:po[p + 1]])
+
+
+def test_build_tracks_device_matches_reference(cuda_ok):
+    """build_tracks_device (all 28 frame pairs matched in one device call, host
+    flow filter + union-find) against the reference's build_tracks(features,
+    default_matcher) on an 8-frame synthetic window: identical tracks."""
+    from gsrecon._bootstrap import build_tracks_device
+    z = np.load(f"{GOLDEN}/tracks.npz")
+    off = z["off"]
+    feats = [(z["kp"][off[f]:off[f + 1]], z["desc"][off[f]:off[f + 1]]) for f in range(len(off) - 1)]
+    tracks = build_tracks_device(feats)
+    flat = np.array([(ti, fr, k, x, y) for ti, tr in enumerate(tracks) for (fr, k, x, y) in tr])
+    np.testing.assert_array_equal(flat, z["tracks"])

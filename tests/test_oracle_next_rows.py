@@ -31,3 +31,21 @@ def test_oracle_match_matches_reference():
         np.testing.assert_array_equal(ia, z["idx_a"][po[p]:po[p + 1]])
         np.testing.assert_array_equal(ib, z["idx_b"][po[p]:po[p + 1]])
         np.testing.assert_array_equal(sc, z["score"][po[p]:po[p + 1]])
+
+
+def test_track_grouping_with_oracle_matcher_matches_reference():
+    """The host half of track building (flow filter + union-find grouping in
+    gsrecon._bootstrap) fed by the oracle matcher reproduces the reference's
+    build_tracks(features, default_matcher) exactly (tests/golden/tracks.npz)."""
+    from gsrecon._bootstrap import build_tracks, filter_matches_flow
+    z = np.load(f"{GOLDEN}/tracks.npz")
+    off = z["off"]
+    feats = [(z["kp"][off[f]:off[f + 1]], z["desc"][off[f]:off[f + 1]]) for f in range(len(off) - 1)]
+
+    def matcher(fa, fb):
+        ia, ib, sc = O.match(fa[1], fb[1])
+        keep = filter_matches_flow(fa[0], fb[0], ia, ib)
+        return ia[keep], ib[keep], sc[keep]
+    tracks = build_tracks(feats, matcher)
+    flat = np.array([(ti, fr, k, x, y) for ti, tr in enumerate(tracks) for (fr, k, x, y) in tr])
+    np.testing.assert_array_equal(flat, z["tracks"])
