@@ -5,7 +5,7 @@
 // (101-132), _assemble (135-177) and solve_step(method="schur") (180-220) --
 // re-mapped so that a problem's whole working set lives in SHARED MEMORY:
 //
-//  * One thread-block cluster of R CTAs per problem (R = 1, 2, 4, 8, 16 chosen
+//  * One thread-block cluster of R CTAs per problem (R = 1, 2, 4, 6, 8, 9, 16 chosen
 //    by the host so the problem fits). CTA r owns a contiguous, point-aligned
 //    slice of the point-major observations; partial normal equations are
 //    summed across the cluster through distributed shared memory (DSMEM) in
@@ -1436,6 +1436,49 @@ struct Plan {
   int R, nt, per_sm;
 };
 
+// Clusters of R CTAs the device keeps resident at once (a cluster must fit in
+// one GPC, so this is not 148 / R). Cached per process (one device per rank).
+template <typename T, int R>
+static int active_clusters_t() {
+  static int cached = -1;
+  if (cached >= 0) return cached;
+  auto kern = solve_v4_kernel<T, R, 256, 1>;
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return cached = 0;
+  const size_t smem = smem_per_cta(1, fa.sharedSizeBytes);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (R > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(R * 1024);
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = R;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  return cached = n;
+}
+
+template <typename T>
+static int active_clusters(int R) {
+  switch (R) {
+    case 8: return active_clusters_t<T, 8>();
+    case 9: return active_clusters_t<T, 9>();
+    case 10: return active_clusters_t<T, 10>();
+    case 12: return active_clusters_t<T, 12>();
+    case 16: return active_clusters_t<T, 16>();
+  }
+  return 0;
+}
+
 // Smallest cluster that fits (every CTA of a cluster repeats the serial
 // phases -- LDL^T, substitutions, step control -- so splitting a problem costs
 // more than it gains; measured on config 4: R=1 247k problems/s (mixed) vs R=2
@@ -1447,8 +1490,37 @@ static Plan plan_t(const MbaBatchDesc* d) {
   const int eP = getenv("MBA_V4_PERSM") ? atoi(getenv("MBA_V4_PERSM")) : 0;
   const int eN = getenv("MBA_V4_NT") ? atoi(getenv("MBA_V4_NT")) : 0;
   const size_t st = 256;   // static shared memory bound
-  for (int R : {1, 2, 4, 8, 16}) {
+  // Clusters are placed inside one GPC (B200: 18-20 SMs each), so a cluster
+  // size that divides a GPC poorly strands SMs: R = 8 runs 2 clusters per GPC
+  // (16 of 18 SMs busy), R = 16 one (16 of 18). For batches that fill the GPU
+  // the planner also tries R = 6 and R = 9 (3 / 2 clusters, 18 SMs busy, and
+  // less per-CTA work than the next power of two); small batches keep the
+  // powers of two, where a larger cluster only shortens the single solve.
+  //
+  // When the smallest fit is R >= 8 on such a batch, every fitting R in
+  // {8, 9, 10, 12, 16} is scored by resident clusters x R / (R + 7): the
+  // second factor models a cluster's solve speed-up with R (serial phases are
+  // repeated per CTA; fitted to config 3 on B200: R = 8 / 9 / 10 / 12 / 16 run
+  // 15 / 15 / 11 / 7 / 7 clusters, best f64 R = 10 at 20.0k problems/s vs
+  // 12.5k at R = 16, best mixed R = 9 at 31.4k vs 29.8k at R = 8).
+  const bool wide = d->n_problems >= 64;
+  if (wide && !eR && !eP && !eN && need_bytes<T>(d, 4) > smem_per_cta(1, st)) {
+    int best = 0;
+    double best_s = 0.0;
+    for (int R : {8, 9, 10, 12, 16}) {
+      if (need_bytes<T>(d, R) > smem_per_cta(1, st)) continue;
+      const double sc = active_clusters<T>(R) * (double)R / (R + 7.0);
+      if (getenv("MBA_DEBUG")) fprintf(stderr, "mba v4 plan score R=%d: %.2f\n", R, sc);
+      if (sc > best_s) {
+        best_s = sc;
+        best = R;
+      }
+    }
+    if (best) return Plan{best, 256, 1};
+  }
+  for (int R : {1, 2, 4, 8, 9, 10, 12, 16}) {
     if (eR && R != eR) continue;
+    if (!eR && (R == 9 || R == 10 || R == 12)) continue;
     for (int per_sm : {2, 1}) {
       if (eP && per_sm != eP) continue;
       if (per_sm == 2 && R > 4) continue;
@@ -1509,6 +1581,11 @@ static int launch_t(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutp
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
+  if (getenv("MBA_DEBUG")) {
+    int ncl = 0;
+    cudaOccupancyMaxActiveClusters(&ncl, kern, &lc);
+    fprintf(stderr, "mba v4 R=%d NT=%d: %d active clusters (%d SMs busy)\n", R, NT, ncl, ncl * R);
+  }
   const cudaError_t err = cudaLaunchKernelEx(&lc, kern, P);
   if (err != cudaSuccess && getenv("MBA_DEBUG"))
     fprintf(stderr, "mba v4 launch (R=%d, NT=%d, smem=%zu): %s\n", R, NT, smem, cudaGetErrorString(err));
@@ -1542,6 +1619,9 @@ static int launch_prec(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaO
     case 2: return launch_t<T, 2, 256, 1>(d, cfg, o, st);
     case 4: return launch_t<T, 4, 256, 1>(d, cfg, o, st);
     case 8: return launch_t<T, 8, 256, 1>(d, cfg, o, st);
+    case 9: return launch_t<T, 9, 256, 1>(d, cfg, o, st);
+    case 10: return launch_t<T, 10, 256, 1>(d, cfg, o, st);
+    case 12: return launch_t<T, 12, 256, 1>(d, cfg, o, st);
     case 16: return launch_t<T, 16, 256, 1>(d, cfg, o, st);
     default: return MBA_ERR_TOO_LARGE;
   }

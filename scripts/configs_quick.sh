@@ -5,7 +5,7 @@ cd "$(dirname "$0")/.."
 for cfg in 1 2 3 5; do
   for prec in f64 mixed; do
     extra=""
-    [ "$cfg" = 3 ] && extra="--problems 256"
+    [ "$cfg" = 3 ] && extra="--problems 1024"
     out=$(MBA_DEBUG=1 timeout 600 python bench.py --config $cfg --precision $prec --steps 3 --warmup 3 --no-e2e --no-cpu-baseline $extra 2>/tmp/err_${cfg}_${prec} | tail -1)
     python - "$cfg" "$prec" "$out" <<'PY'
 import json, sys

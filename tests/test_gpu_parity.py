@@ -201,6 +201,33 @@ def test_cluster_kernel_plans(cuda_ok):
     assert solver.plan(big, solver.LmParams(precision="mixed")) == 8
 
 
+@pytest.mark.parametrize("R", [9, 10, 12])
+@pytest.mark.parametrize("precision", ["mixed", "f64"])
+def test_non_power_of_two_clusters(R, precision, cuda_ok, monkeypatch):
+    """Cluster sizes that tile a GPC better (9/10/12 CTAs, chosen for full
+    batches of large problems) split observations at point boundaries and sum
+    through DSMEM exactly like the power-of-two plans: oracle parity, and the
+    default one-CTA plan reaches the same final costs."""
+    from paper_2506_05558_b200 import solver
+    from paper_2506_05558_b200.synth import make_batch
+    b = make_batch(4, n_cams=8, K=3000, seed=31)
+    probs = [b.problem(i) for i in range(4)]
+    cfg = dict(max_iters=200)
+    base = run_device(probs, cfg, precision, "v4")
+    monkeypatch.setenv("MBA_V4_R", str(R))
+    assert solver.plan(solver.to_device(solver.pack_problems(probs)),
+                       solver.LmParams(precision=precision)) == R
+    dev = run_device(probs, cfg, precision, "v4")
+    for i in range(4):
+        assert dev[i]["status"] == base[i]["status"]
+        np.testing.assert_allclose(dev[i]["costs"][-1], base[i]["costs"][-1], rtol=1e-6)
+    for i in (0, 3):
+        q = b.problem(i)                 # the oracle rebinds q's R, t, focal, points
+        ref = O.lm(q, max_iters=200)
+        assert_parity(dev[i], ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"],
+                      q["R"], q["t"], q["focal"], label=f"R{R}[{i}]")
+
+
 def test_plan_overflow_is_resolved_by_cta_kernel(cuda_ok, monkeypatch):
     """Problems whose slice does not fit the cluster kernel's shared-memory
     plan are flagged and re-solved by the CTA kernel in the same mba_solve:
