@@ -1255,6 +1255,25 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         if (lane + 32 < C) { dc[lane + 32] = (double)u1; dcT[lane + 32] = u1; }
       }
       __syncthreads();
+      // trial cameras of all five tries (R <- exp(frac dw) R, t + frac dt,
+      // miniba.py:264-266), by the highest-numbered threads, overlapped with
+      // the point back substitution (the barrier after it publishes both)
+      for (int q = NT - 1 - tid; q < kBacktrackTries * n; q += NT) {
+        const int bt = q / n, c = q % n, s = slot[c];
+        const double frac = ldexp(1.0, -bt);
+        double* Rq = Rt + (size_t)(bt * n + c) * 9;
+        double* tq = tt + (size_t)(bt * n + c) * 3;
+        if (s < 0) {
+          for (int i = 0; i < 9; ++i) Rq[i] = Rc[9 * c + i];
+          for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i];
+        } else {
+          double w[3] = {frac * dc[6 * s], frac * dc[6 * s + 1], frac * dc[6 * s + 2]};
+          double E[9];
+          exp_so3(w, E);
+          matmul33(E, Rc + 9 * c, Rq);
+          for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i] + frac * dc[6 * s + 3 + i];
+        }
+      }
       // point back substitution (miniba.py:216-217): dp = -L^-T (z + yf df + sum Y_i^T dc_a)
       if (opt_pts) {
         const T df = has_f ? dcT[FI] : T(0);
@@ -1304,23 +1323,6 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     double tc_[3] = {0, 0, 0};
     double ft = f;
     if (!chol_fail) {
-      for (int q = tid; q < kBacktrackTries * n; q += NT) {
-        const int bt = q / n, c = q % n, s = slot[c];
-        const double frac = ldexp(1.0, -bt);
-        double* Rq = Rt + (size_t)(bt * n + c) * 9;
-        double* tq = tt + (size_t)(bt * n + c) * 3;
-        if (s < 0) {
-          for (int i = 0; i < 9; ++i) Rq[i] = Rc[9 * c + i];
-          for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i];
-        } else {
-          double w[3] = {frac * dc[6 * s], frac * dc[6 * s + 1], frac * dc[6 * s + 2]};
-          double E[9];
-          exp_so3(w, E);
-          matmul33(E, Rc + 9 * c, Rq);
-          for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i] + frac * dc[6 * s + 3 + i];
-        }
-      }
-      __syncthreads();
       // try 0 (the full step) alone; if it is rejected, tries 1..4 in one
       // fused pass. `tries` keeps the reference's count (first accepted try + 1,
       // or 5), miniba.py:262-276.

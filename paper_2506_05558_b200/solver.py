@@ -272,14 +272,23 @@ def descriptors(db: DeviceBatch, prm: LmParams, sol: Solution):
     return d, c, o
 
 
-def solve(db: DeviceBatch, prm: LmParams, sol: Solution | None = None) -> Solution:
-    """Enqueue mba_solve on the current stream (asynchronous)."""
+def workspace_bytes(db: DeviceBatch, prm: LmParams) -> int:
+    """Device workspace mba_solve needs for this batch (mba_workspace_bytes)."""
+    d, c = _desc(db, prm)
+    return int(_lib.lib().mba_workspace_bytes(ct.byref(d), ct.byref(c)))
+
+
+def solve(db: DeviceBatch, prm: LmParams, sol: Solution | None = None, ws=None) -> Solution:
+    """Enqueue mba_solve on the current stream (asynchronous). `ws`: a caller-
+    owned uint8 workspace (needed when solves run concurrently on several
+    streams); default: one shared per-device workspace."""
     L = _lib.lib()
     if sol is None:
         sol = Solution(db, prm.max_iters)
     d, c, o = descriptors(db, prm, sol)
     nbytes = L.mba_workspace_bytes(ct.byref(d), ct.byref(c))
-    ws = _workspace(nbytes, db.obs.device)
+    if ws is None or ws.numel() < nbytes:
+        ws = _workspace(nbytes, db.obs.device)
     rc = L.mba_solve(ct.byref(d), ct.byref(c), ct.byref(o), ptr(ws), ws.numel(), _lib.stream_ptr())
     _lib.check(rc, "mba_solve")
     return sol
@@ -347,7 +356,10 @@ def split_host_batch(hb: HostBatch, n_chunks: int):
 class PipelinedSolver:
     """End-to-end solve of a host batch: H2D of chunk i+1 overlaps the solve
     of chunk i on a second stream; each chunk's solution (R, t, focal, points,
-    final stats, n_iters, status) is copied back to pinned host memory."""
+    final stats, n_iters, status) is copied back to pinned host memory.
+    Chunk solves alternate between two compute streams (each chunk has its own
+    workspace), so the next chunk's problems fill the SMs the previous chunk's
+    last problems leave idle instead of waiting for its tail."""
 
     OUT = ("R", "t", "focal", "points", "final_stats", "n_iters", "status")
 
@@ -358,45 +370,62 @@ class PipelinedSolver:
         self.pinned = [pin(p) for p in self.parts]
         self.copy = torch.cuda.Stream()      # host -> device
         self.compute = torch.cuda.Stream()
+        self.compute2 = torch.cuda.Stream()
         self.back = torch.cuda.Stream()      # device -> host (own stream: a chunk's read-back
         #                                      must not hold up the next chunk's upload)
         self.dev = [to_device(p, pinned=self.pinned[i]) for i, p in enumerate(self.parts)]
         torch.cuda.synchronize()
         self.sols = [Solution(d, prm.max_iters) for d in self.dev]
+        self.ws = [torch.empty(max(workspace_bytes(d, prm), 16), dtype=torch.uint8, device=d.obs.device)
+                   for d in self.dev]
         self.host = [{k: torch.empty(getattr(s, k).shape, dtype=getattr(s, k).dtype, pin_memory=True)
                       for k in self.OUT} for s in self.sols]
         self.h2d_bytes = sum(d.h2d_bytes for d in self.dev)
         self.d2h_bytes = sum(v.numel() * v.element_size() for h in self.host for v in h.values())
 
     def run(self):
-        """Enqueue H2D -> solve -> D2H for every chunk (asynchronous)."""
+        """Enqueue H2D -> solve -> D2H for every chunk (asynchronous).
+
+        Consecutive runs pipeline per chunk: run n+1's upload of chunk i waits
+        only for run n's solve of chunk i (it overwrites that chunk's device
+        inputs) and its solve of chunk i for run n's read-back of chunk i (it
+        overwrites the outputs), so the next run's first uploads overlap this
+        run's last solves instead of waiting for the whole run."""
         torch = _lib.torch_cuda()
         fields = _INPUT_FIELDS
+        if not hasattr(self, "_solved"):
+            self._solved = [None] * len(self.dev)
+            self._read = [None] * len(self.dev)
         for i, (d, src) in enumerate(zip(self.dev, self.pinned)):
+            if self._solved[i] is not None:
+                self.copy.wait_event(self._solved[i])
             with torch.cuda.stream(self.copy):
                 for k in fields:
                     if src[k] is not None:
                         getattr(d, k).copy_(src[k], non_blocking=True)
                 h2d = torch.cuda.Event()
                 h2d.record(self.copy)
-            self.compute.wait_event(h2d)
-            with torch.cuda.stream(self.compute):
-                solve(d, self.prm, self.sols[i])
+            cs = self.compute if i % 2 == 0 else self.compute2
+            cs.wait_event(h2d)
+            if self._read[i] is not None:
+                cs.wait_event(self._read[i])
+            with torch.cuda.stream(cs):
+                solve(d, self.prm, self.sols[i], ws=self.ws[i])
                 done = torch.cuda.Event()
-                done.record(self.compute)
+                done.record(cs)
+            self._solved[i] = done
             self.back.wait_event(done)
             with torch.cuda.stream(self.back):
                 for k in self.OUT:
                     self.host[i][k].copy_(getattr(self.sols[i], k), non_blocking=True)
-        # the next run's uploads overwrite the device inputs and its solves the
-        # device outputs: order them after this run's solves and read-backs
-        self.copy.wait_stream(self.compute)
-        self.copy.wait_stream(self.back)
+                rd = torch.cuda.Event()
+                rd.record(self.back)
+            self._read[i] = rd
         return self
 
     def wait(self):
         """Make the current stream wait for every copy and solve of run()."""
         torch = _lib.torch_cuda()
         cur = torch.cuda.current_stream()
-        for s_ in (self.copy, self.compute, self.back):
+        for s_ in (self.copy, self.compute, self.compute2, self.back):
             cur.wait_stream(s_)
