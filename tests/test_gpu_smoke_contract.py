@@ -116,3 +116,29 @@ def test_reference_smoke_script_runs_unchanged(cuda_ok):
     assert "ALL MINIBA SMOKE CHECKS PASSED" in r.stdout
     # it must have exercised this package, not the reference
     assert f"GSRECON_FROM {os.path.join(REPO, 'src', 'gsrecon', 'miniba.py')}" in r.stdout
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_on_one_gpu(tmp_path):
+    """The N-rank bench flow (torchrun, contiguous shards, max-over-ranks
+    timing, final gather) end to end with 2 ranks; on this one-GPU box both
+    ranks share GPU 0 and the collectives go over gloo (MBA_BENCH_ONE_GPU)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MBA_BENCH_ONE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2",
+           "--problems", "512", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]   # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["n_problems"] == 512
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] >= 1
+    os.makedirs(os.path.join(repo, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(repo, "gpurun_out", "bench_two_ranks.json"), "w") as fh:
+        fh.write(lines[0] + "\n")
