@@ -199,6 +199,11 @@ def test_cluster_kernel_plans(cuda_ok):
     assert solver.plan(small, solver.LmParams(precision="mixed")) == 1
     assert solver.plan(big, solver.LmParams(precision="f64")) == 16
     assert solver.plan(big, solver.LmParams(precision="mixed")) == 8
+    # a full batch of config-3 problems: the planner scores the fitting cluster
+    # sizes by resident clusters (B200: 10 in f64, 9 in mixed)
+    full = solver.to_device(solver.pack_synth(make_batch(64, n_cams=8, K=20000, seed=3)))
+    assert solver.plan(full, solver.LmParams(precision="f64")) in (10, 12, 16)
+    assert solver.plan(full, solver.LmParams(precision="mixed")) in (8, 9, 10, 12, 16)
 
 
 @pytest.mark.parametrize("R", [9, 10, 12])
