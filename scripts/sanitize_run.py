@@ -1,5 +1,5 @@
 """Small workloads for compute-sanitizer: the cluster-resident solver (f64 and
-mixed, R = 1 and a 16-CTA cluster, overflow re-solve), pose LM, triangulation
+mixed, R = 1, a 16-CTA and a 10-CTA cluster, overflow re-solve), pose LM, triangulation
 and matching."""
 import os
 import sys
@@ -20,6 +20,10 @@ def main():
         run_device(probs, dict(max_iters=8), prec, "auto")
     big = make_batch(1, n_cams=6, K=9000, seed=5).problem(0)
     run_device([big], dict(max_iters=4), "f64", "auto")      # cluster of CTAs
+    os.environ["MBA_V4_R"] = "10"                             # non-power-of-two cluster
+    run_device([big], dict(max_iters=4), "f64", "auto")
+    run_device([big], dict(max_iters=4), "mixed", "auto")
+    del os.environ["MBA_V4_R"]
     os.environ["MBA_V4_ARENA_CAP"] = "20000"
     run_device(probs[:1], dict(max_iters=4), "f64", "auto")  # overflow -> CTA kernel
     del os.environ["MBA_V4_ARENA_CAP"]
