@@ -10,7 +10,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libminiba.so")
 LIB_PROF = os.path.join(HERE, "libminiba_prof.so")
-SOURCES = ["mba_solve.cu", "mba_v4.cu", "mba_stages.cu", "mba_pose.cu", "mba_tri.cu", "mba_match.cu"]
+# (source, extra defines, object): the cluster kernel is built once per arithmetic type
+SOURCES = [("mba_solve.cu", [], "mba_solve.o"), ("mba_v4.cu", [], "mba_v4_f64.o"),
+           ("mba_v4.cu", ["-DMBA_V4_F32"], "mba_v4_f32.o"), ("mba_stages.cu", [], "mba_stages.o"),
+           ("mba_pose.cu", [], "mba_pose.o"), ("mba_tri.cu", [], "mba_tri.o"),
+           ("mba_match.cu", [], "mba_match.o")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -30,17 +34,23 @@ def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str
     lib = LIB_PROF if prof else LIB
     if not force and not prof and not _stale():
         return LIB
-    objs = []
-    log = []
-    for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, *(["-DMBA_PHASE_PROF"] if prof else []), "-c",
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(job):
+        src, defs, obj = job
+        obj = os.path.join(CSRC, obj)
+        cmd = [NVCC, *FLAGS, *defs, *(["-DMBA_PHASE_PROF"] if prof else []), "-c",
                os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-        objs.append(obj)
+        return obj, r.stderr
+
+    # one nvcc per translation unit, in parallel (the big units dominate)
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        res = list(ex.map(compile_one, SOURCES))
+    objs = [o for o, _ in res]
+    log = [e for _, e in res]
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib, *objs,
            "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)

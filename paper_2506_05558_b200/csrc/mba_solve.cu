@@ -948,1279 +948,6 @@ __global__ void __launch_bounds__(NT, MINB) solve_kernel(SolveParams P) {
   }
 }
 
-// ===========================================================================
-// Warp-per-problem solver for batches of small problems (<= 8 cameras).
-//
-// Same algorithm and arithmetic as solve_one, re-mapped so that ONE WARP owns
-// a whole problem: lanes stride over points / observations / pairs, every
-// reduction is a warp butterfly, and the only synchronisation is __syncwarp.
-// With 8-16 independent problems per SM there are no block barriers on the
-// critical path and the warps hide each other's memory latency. The reduced
-// camera system is stored column-major packed (column k contiguous), so the
-// LDL^T and both substitutions stream columns.
-// ===========================================================================
-
-constexpr int kWarpsPerCta = 4;
-
-template <typename T, int MAXC>
-struct WLayout {
-  static constexpr int N = MAXC, C = 6 * MAXC + 1, NB = MAXC * (MAXC + 1) / 2, CC = C * (C + 1) / 2;
-  static constexpr size_t oRc = 0;
-  static constexpr size_t oTc = oRc + 8 * 9 * N;
-  static constexpr size_t oRt = oTc + 8 * 3 * N;
-  static constexpr size_t oTt = oRt + 8 * 9 * N;
-  static constexpr size_t oDc = oTt + 8 * 3 * N;
-  static constexpr size_t oS = align16(oDc + 8 * C);
-  static constexpr size_t oRhs = align16(oS + sizeof(T) * CC);
-  static constexpr size_t oUcam = align16(oRhs + sizeof(T) * C);
-  static constexpr size_t oCamPtr = align16(oUcam + sizeof(T) * N * kUcamStride);
-  static constexpr size_t oSlot = oCamPtr + 4 * (N + 1);
-  static constexpr size_t oCos = oSlot + 4 * N;
-  static constexpr size_t oBlkOff = oCos + 4 * N;
-  static constexpr size_t oBlkA = oBlkOff + 4 * (NB + 1);
-  static constexpr size_t oBlkB = oBlkA + NB;
-  static constexpr size_t kBytes = align16(oBlkB + NB);
-};
-
-// column-major packed lower: entry (i >= j) at colstart(j) + i - j
-__device__ __forceinline__ int colstart(int j, int C) { return j * C - (j * (j - 1)) / 2; }
-
-template <typename T>
-__device__ void warp_cost_pass(const MbaObs* __restrict__ obs, const float* __restrict__ lo, int K,
-                               const double* __restrict__ X, const T* __restrict__ ptw, double frac,
-                               bool use_dp, const double* Rs, const double* ts, double f, double cx,
-                               double cy, double delta, int loss, int lane, double out[3]) {
-  constexpr int U = 4;
-  double acc[3] = {0.0, 0.0, 0.0};
-  for (int k0 = lane; k0 < K; k0 += U * 32) {
-    Obs o[U];
-    double Xp[U][3];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = k0 + u * 32;
-      if (k < K) o[u] = load_obs(obs, lo, k);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = k0 + u * 32;
-      if (k >= K) continue;
-      const double* x = X + 3 * o[u].pt;
-      Xp[u][0] = x[0];
-      Xp[u][1] = x[1];
-      Xp[u][2] = x[2];
-      if (use_dp) {
-        const T* dp = ptw + (size_t)o[u].pt * kPtStride + 12;
-        Xp[u][0] = Xp[u][0] + frac * (double)dp[0];
-        Xp[u][1] = Xp[u][1] + frac * (double)dp[1];
-        Xp[u][2] = Xp[u][2] + frac * (double)dp[2];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = k0 + u * 32;
-      if (k >= K) continue;
-      Proj pr = project_residual_fast(Rs + 9 * o[u].cam, ts + 3 * o[u].cam, Xp[u], f, cx, cy, o[u].u, o[u].v);
-      const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
-      acc[0] += robust_rho(e, delta, loss);
-      acc[1] += e;
-      acc[2] += e * e;
-    }
-  }
-  out[0] = warp_sum(acc[0]);
-  out[1] = warp_sum(acc[1]);
-  out[2] = warp_sum(acc[2]);
-}
-
-template <typename T, int MAXC>
-__device__ void warp_solve_one(const SolveParams& P, int b, unsigned char* sbase,
-                               const Scratch<T, false>& W) {
-  using L = WLayout<T, MAXC>;
-  constexpr unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const MbaBatchDesc& D = P.d;
-  const MbaLmConfig& cfg = P.cfg;
-  const MbaOutputs& O = P.o;
-  double* Rc = (double*)(sbase + L::oRc);
-  double* tc = (double*)(sbase + L::oTc);
-  double* Rt = (double*)(sbase + L::oRt);
-  double* tt = (double*)(sbase + L::oTt);
-  double* dcs = (double*)(sbase + L::oDc);
-  T* S = (T*)(sbase + L::oS);
-  T* rhs = (T*)(sbase + L::oRhs);
-  T* ucam = (T*)(sbase + L::oUcam);
-  int* cam_ptr = (int*)(sbase + L::oCamPtr);
-  int* slot = (int*)(sbase + L::oSlot);
-  int* cam_of_slot = (int*)(sbase + L::oCos);
-  int* blk_off = (int*)(sbase + L::oBlkOff);
-  unsigned char* blk_a = sbase + L::oBlkA;
-  unsigned char* blk_b = sbase + L::oBlkB;
-
-  const int64_t cb = D.cam_off[b], pb = D.pt_off[b], ob = D.obs_off[b];
-  const int n = (int)(D.cam_off[b + 1] - cb);
-  const int Pn = (int)(D.pt_off[b + 1] - pb);
-  const int K = (int)(D.obs_off[b + 1] - ob);
-  const uint8_t fl = D.flags[b];
-  const bool has_f = fl & 1, opt_pts = (fl >> 1) & 1;
-  const double cx = D.cx[b], cy = D.cy[b];
-  const double delta = cfg.delta, nu = cfg.nu;
-  const int loss = cfg.loss, max_it = cfg.max_iters;
-  const MbaObs* __restrict__ obs = D.obs + ob;
-  const float* __restrict__ lo = D.obs_lo ? D.obs_lo + 2 * ob : nullptr;
-  double* __restrict__ X = O.points_out + 3 * pb;
-  int* __restrict__ perm = W.perm;
-  int* __restrict__ ptr = W.ptr;
-  T* __restrict__ Ybuf = W.Ybuf;
-  T* __restrict__ ptw = W.ptw;
-  constexpr int YSTR = kYStride;  // (warp kernel: global scratch, int indices)
-  double* costs = O.costs + (size_t)b * (max_it + 1);
-  double* lambdas = O.lambdas + (size_t)b * max_it;
-  uint8_t* accepted = O.accepted + (size_t)b * max_it;
-  uint8_t* evals = O.evals + (size_t)b * max_it;
-
-  // ---------------- setup ----------------
-  for (int i = lane; i < n * 9; i += 32) Rc[i] = O.R_in[cb * 9 + i];
-  for (int i = lane; i < n * 3; i += 32) tc[i] = O.t_in[cb * 3 + i];
-  if (O.points_in != O.points_out)
-    for (int i = lane; i < Pn * 3; i += 32) X[i] = O.points_in[pb * 3 + i];
-  const bool is_free = lane < n && !D.fixed[cb + lane];
-  const unsigned free_mask = __ballot_sync(FULL, is_free);
-  const int nf = __popc(free_mask);
-  if (lane < n) slot[lane] = is_free ? __popc(free_mask & ((1u << lane) - 1u)) : -1;
-  if (is_free) cam_of_slot[__popc(free_mask & ((1u << lane) - 1u))] = lane;
-  const int C = 6 * nf + (has_f ? 1 : 0), FI = C - 1;
-  const int nb = opt_pts ? nf * (nf + 1) / 2 : 0;
-  if (lane == 0) {
-    int q = 0;
-    for (int a = 0; a < nf; ++a)
-      for (int bb = a; bb < nf; ++bb, ++q) {
-        blk_a[q] = (unsigned char)a;
-        blk_b[q] = (unsigned char)bb;
-      }
-  }
-  for (int p = lane; p <= Pn; p += 32) {
-    int lo_i = 0, hi_i = K;
-    while (lo_i < hi_i) {
-      int mid = (lo_i + hi_i) >> 1;
-      if (__ldg(&obs[mid].pt) < p) lo_i = mid + 1; else hi_i = mid;
-    }
-    ptr[p] = lo_i;
-  }
-  bool bad = false;
-  for (int k = lane; k < K; k += 32) {
-    int pt = __ldg(&obs[k].pt), c = __ldg(&obs[k].cam);
-    bad |= pt < 0 || pt >= Pn || c < 0 || c >= n || (k > 0 && __ldg(&obs[k - 1].pt) > pt);
-  }
-  bad = __any_sync(FULL, bad);
-  if (lane == 0) cam_ptr[0] = 0;
-  for (int c = 0; c < n; ++c) {
-    int cnt = 0;
-    for (int k0 = 0; k0 < K; k0 += 32) {
-      const int k = k0 + lane;
-      cnt += __popc(__ballot_sync(FULL, k < K && obs_cam(obs, k) == c));
-    }
-    if (lane == 0) cam_ptr[c + 1] = cam_ptr[c] + cnt;
-    __syncwarp();
-  }
-  for (int c = 0; c < n; ++c) {
-    int base = cam_ptr[c];
-    for (int k0 = 0; k0 < K; k0 += 32) {
-      const int k = k0 + lane;
-      const bool hit = k < K && obs_cam(obs, k) == c;
-      const unsigned m = __ballot_sync(FULL, hit);
-      if (hit) perm[base + __popc(m & ((1u << lane) - 1u))] = k;
-      base += __popc(m);
-    }
-  }
-  __syncwarp();
-  if (lane == 0) blk_off[0] = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int blk = 0; blk < nb; ++blk) {
-      const int ca = cam_of_slot[blk_a[blk]], cbb = cam_of_slot[blk_b[blk]];
-      const int q1 = cam_ptr[ca + 1];
-      int base = pass ? blk_off[blk] : 0;
-      for (int q0 = cam_ptr[ca]; q0 < q1; q0 += 32) {
-        const int q = q0 + lane;
-        int i = -1, j0 = 0, j1 = 0, m = 0;
-        if (q < q1) {
-          i = perm[q];
-          const int pt = __ldg(&obs[i].pt);
-          j0 = ptr[pt];
-          j1 = ptr[pt + 1];
-          for (int j = j0; j < j1; ++j) m += obs_cam(obs, j) == cbb;
-        }
-        if (pass) {
-          int pos = base + warp_excl_scan(m, lane);
-          for (int j = j0; j < j1 && m; ++j)
-            if (obs_cam(obs, j) == cbb) W.set_pair(pos++, i, j);
-        }
-        base += warp_sum(m);
-      }
-      if (!pass && lane == 0) blk_off[blk + 1] = blk_off[blk] + base;
-      __syncwarp();
-    }
-  }
-  double f = O.focal_in[b];
-  if (bad) {
-    if (lane == 0) {
-      O.n_iters[b] = 0;
-      O.status[b] = -1;
-      O.focal_out[b] = f;
-    }
-    for (int i = lane; i < n * 9; i += 32) O.R_out[cb * 9 + i] = Rc[i];
-    for (int i = lane; i < n * 3; i += 32) O.t_out[cb * 3 + i] = tc[i];
-    __syncwarp();
-    return;
-  }
-  __syncwarp();
-
-  double st[3];
-  warp_cost_pass<T>(obs, lo, K, X, ptw, 0.0, false, Rc, tc, f, cx, cy, delta, loss, lane, st);
-  double cost = st[0], se = st[1], se2 = st[2];
-  double lam = cfg.lambda_init;
-  if (lane == 0) costs[0] = cost;
-  int it = 0, stop_reason = MBA_SOLVE_MAX_ITERS;
-
-  for (; it < max_it;) {
-    const T tlam = T(lam);
-    // ---------- K1+K2 point pass (lane per point) ----------
-    T part[4] = {T(0), T(0), T(0), T(0)};
-    for (int p = lane; p < Pn; p += 32) {
-      const double Xp[3] = {X[3 * p], X[3 * p + 1], X[3 * p + 2]};
-      const int k0 = ptr[p], k1 = ptr[p + 1];
-      T V[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
-      T g[3] = {T(0), T(0), T(0)}, wf[3] = {T(0), T(0), T(0)};
-      for (int k = k0; k < k1; ++k) {
-        Obs o = load_obs(obs, lo, k);
-        const double* Rk = Rc + 9 * o.cam;
-        Proj pr = project_residual_fast(Rk, tc + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
-        const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
-        const T w = T(robust_w(e, delta, loss));
-        T A[12], Fb[2], Bm[6];
-        jac_blocks<T>(pr, Rk, f, A, Fb, Bm);
-        const T r0 = T(pr.ru), r1 = T(pr.rv);
-        T wB[6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) wB[i] = w * Bm[i];
-        if (has_f) {
-          part[0] += w * (Fb[0] * Fb[0] + Fb[1] * Fb[1]);
-          part[1] += w * (Fb[0] * r0 + Fb[1] * r1);
-        }
-        if (opt_pts) {
-          V[0] += Bm[0] * wB[0] + Bm[3] * wB[3];
-          V[1] += Bm[1] * wB[0] + Bm[4] * wB[3];
-          V[2] += Bm[1] * wB[1] + Bm[4] * wB[4];
-          V[3] += Bm[2] * wB[0] + Bm[5] * wB[3];
-          V[4] += Bm[2] * wB[1] + Bm[5] * wB[4];
-          V[5] += Bm[2] * wB[2] + Bm[5] * wB[5];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) g[a] += wB[a] * r0 + wB[3 + a] * r1;
-          if (has_f) {
-            const T wf0 = w * Fb[0], wf1 = w * Fb[1];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) wf[a] += wf0 * Bm[a] + wf1 * Bm[3 + a];
-          }
-          if (slot[o.cam] >= 0) {
-            T Wm[18];
-#pragma unroll
-            for (int r = 0; r < 6; ++r)
-#pragma unroll
-              for (int a = 0; a < 3; ++a) Wm[r * 3 + a] = A[r] * wB[a] + A[6 + r] * wB[3 + a];
-            store18(Ybuf + (size_t)k * YSTR, Wm);
-          }
-        }
-      }
-      if (!opt_pts) continue;
-      V[0] += tlam * (V[0] > T(kDiagFloor) ? V[0] : T(kDiagFloor));
-      V[2] += tlam * (V[2] > T(kDiagFloor) ? V[2] : T(kDiagFloor));
-      V[5] += tlam * (V[5] > T(kDiagFloor) ? V[5] : T(kDiagFloor));
-      const T L00 = sqrt(V[0]);
-      const T i00 = T(1) / L00;
-      const T L10 = V[1] * i00, L20 = V[3] * i00;
-      const T L11 = sqrt(V[2] - L10 * L10);
-      const T i11 = T(1) / L11;
-      const T L21 = (V[4] - L20 * L10) * i11;
-      const T L22 = sqrt(V[5] - L20 * L20 - L21 * L21);
-      const T i22 = T(1) / L22;
-      for (int k = k0; k < k1; ++k) {
-        if (slot[obs_cam(obs, k)] < 0) continue;
-        T* Wk = Ybuf + (size_t)k * YSTR;
-        T y[18];
-        load18(Wk, y);
-#pragma unroll
-        for (int r = 0; r < 6; ++r) {
-          const T y0 = y[r * 3 + 0] * i00;
-          const T y1 = (y[r * 3 + 1] - L10 * y0) * i11;
-          const T y2 = (y[r * 3 + 2] - L20 * y0 - L21 * y1) * i22;
-          y[r * 3 + 0] = y0;
-          y[r * 3 + 1] = y1;
-          y[r * 3 + 2] = y2;
-        }
-        store18(Wk, y);
-      }
-      const T z0 = g[0] * i00, z1 = (g[1] - L10 * z0) * i11, z2 = (g[2] - L20 * z0 - L21 * z1) * i22;
-      const T f0 = wf[0] * i00, f1 = (wf[1] - L10 * f0) * i11, f2 = (wf[2] - L20 * f0 - L21 * f1) * i22;
-      part[2] += f0 * f0 + f1 * f1 + f2 * f2;
-      part[3] += f0 * z0 + f1 * z1 + f2 * z2;
-      T* pw = ptw + (size_t)p * kPtStride;
-      pw[0] = L00; pw[1] = L10; pw[2] = L11; pw[3] = L20; pw[4] = L21; pw[5] = L22;
-      pw[6] = z0; pw[7] = z1; pw[8] = z2;
-      pw[9] = f0; pw[10] = f1; pw[11] = f2;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) part[i] = warp_sum(part[i]);
-    __syncwarp();  // Y and point factors written by other lanes are visible
-
-    // ---------- K2 camera jobs ----------
-    for (int s = 0; s < nf; ++s) {
-      const int c = cam_of_slot[s];
-      const double* Rk = Rc + 9 * c;
-      T acc[kUcamStride];
-#pragma unroll
-      for (int i = 0; i < kUcamStride; ++i) acc[i] = T(0);
-      for (int q = cam_ptr[c] + lane; q < cam_ptr[c + 1]; q += 32) {
-        const int k = perm[q];
-        Obs o = load_obs(obs, lo, k);
-        const double Xp[3] = {X[3 * o.pt], X[3 * o.pt + 1], X[3 * o.pt + 2]};
-        Proj pr = project_residual_fast(Rk, tc + 3 * c, Xp, f, cx, cy, o.u, o.v);
-        const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
-        const T w = T(robust_w(e, delta, loss));
-        T A[12], Fb[2], Bm[6];
-        jac_blocks<T>(pr, Rk, f, A, Fb, Bm);
-        const T r0 = T(pr.ru), r1 = T(pr.rv);
-        int idx = 0;
-#pragma unroll
-        for (int r = 0; r < 6; ++r) {
-          const T wa0 = w * A[r], wa1 = w * A[6 + r];
-#pragma unroll
-          for (int cc = 0; cc <= r; ++cc) acc[idx++] += wa0 * A[cc] + wa1 * A[6 + cc];
-          acc[21 + r] += wa0 * Fb[0] + wa1 * Fb[1];
-          acc[27 + r] += wa0 * r0 + wa1 * r1;
-        }
-        if (opt_pts) {
-          T y[18];
-          load18(Ybuf + (size_t)k * YSTR, y);
-          const T* pw = ptw + (size_t)o.pt * kPtStride;
-          const T z0 = pw[6], z1 = pw[7], z2 = pw[8], f0 = pw[9], f1 = pw[10], f2 = pw[11];
-#pragma unroll
-          for (int r = 0; r < 6; ++r) {
-            acc[33 + r] += y[r * 3] * f0 + y[r * 3 + 1] * f1 + y[r * 3 + 2] * f2;
-            acc[39 + r] += y[r * 3] * z0 + y[r * 3 + 1] * z1 + y[r * 3 + 2] * z2;
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < kUcamStride; ++i) acc[i] = warp_sum(acc[i]);
-      // every lane holds the totals; lanes store disjoint entries
-#pragma unroll
-      for (int i = 0; i < kUcamStride; ++i)
-        if ((i & 31) == lane) ucam[s * kUcamStride + i] = acc[i];
-    }
-    // ---------- K3 pair jobs: S_ab = -sum Y_i Y_j^T ----------
-    for (int blk = 0; blk < nb; ++blk) {
-      const int sa = blk_a[blk], sb = blk_b[blk];
-      T acc[36];
-#pragma unroll
-      for (int i = 0; i < 36; ++i) acc[i] = T(0);
-      const int q1 = blk_off[blk + 1];
-      for (int q = blk_off[blk] + lane; q < q1; q += 32) {
-        const int2 pr = W.pair(q);
-        T yi[18], yj[18];
-        load18(Ybuf + (size_t)pr.x * YSTR, yi);
-        load18(Ybuf + (size_t)pr.y * YSTR, yj);
-#pragma unroll
-        for (int r = 0; r < 6; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 6; ++cc)
-            acc[r * 6 + cc] += yi[r * 3] * yj[cc * 3] + yi[r * 3 + 1] * yj[cc * 3 + 1] +
-                               yi[r * 3 + 2] * yj[cc * 3 + 2];
-      }
-#pragma unroll
-      for (int i = 0; i < 36; ++i) acc[i] = warp_sum(acc[i]);
-      // column-major packed: rows of sb (>= columns of sa)
-#pragma unroll
-      for (int i = 0; i < 36; ++i) {
-        if ((i & 31) != lane) continue;
-        const int r = i / 6, cc = i % 6;   // acc[r][cc] = (row 6sa+r, col 6sb+cc)
-        const int row = 6 * sb + cc, col = 6 * sa + r;  // transpose into the lower triangle
-        if (sa == sb && cc < r) continue;               // diagonal block: keep the lower half
-        S[colstart(col, C) + row - col] = -acc[i];
-      }
-    }
-    __syncwarp();
-
-    // ---------- assemble damped S and rhs ----------
-    if (!opt_pts)
-      for (int i = lane; i < C * (C + 1) / 2; i += 32) S[i] = T(0);
-    __syncwarp();
-    if (lane < nf) {
-      const int s = lane;
-      const T* u = ucam + s * kUcamStride;
-      int idx = 0;
-      for (int r = 0; r < 6; ++r) {
-        for (int cc = 0; cc <= r; ++cc, ++idx) {
-          T ud = u[idx];
-          if (r == cc) ud += tlam * (ud > T(kDiagFloor) ? ud : T(kDiagFloor));
-          const int row = 6 * s + r, col = 6 * s + cc;
-          S[colstart(col, C) + row - col] += ud;
-        }
-        if (has_f) S[colstart(6 * s + r, C) + FI - (6 * s + r)] = u[21 + r] - (opt_pts ? u[33 + r] : T(0));
-        rhs[6 * s + r] = -u[27 + r] + (opt_pts ? u[39 + r] : T(0));
-      }
-    }
-    if (has_f && lane == 0) {
-      const T uff = part[0];
-      const T ud = uff + tlam * (uff > T(kDiagFloor) ? uff : T(kDiagFloor));
-      S[colstart(FI, C)] = ud - part[2];
-      rhs[FI] = -part[1] + part[3];
-    }
-    __syncwarp();
-
-    // ---------- K4 LDL^T (column-major, lane per trailing column) ----------
-    bool chol_fail = false;
-    for (int k = 0; k < C; ++k) {
-      const T* colk = S + colstart(k, C) - k;   // colk[i] = S[i][k], i >= k
-      const T d = colk[k];
-      if (!(d > T(0)) || !isfinite((double)d)) {
-        chol_fail = true;
-        break;
-      }
-      const T inv = T(1) / d;
-      for (int j = k + 1 + lane; j < C; j += 32) {
-        const T ljk = colk[j] * inv;
-        T* colj = S + colstart(j, C) - j;
-        for (int i = j; i < C; ++i) colj[i] -= colk[i] * ljk;
-      }
-      __syncwarp();
-    }
-    if (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull)) chol_fail = true;
-
-    if (!chol_fail) {
-      // forward (unit L): rhs_i -= L_ik d_k * (rhs_k / d_k)
-      for (int k = 0; k < C; ++k) {
-        const T* colk = S + colstart(k, C) - k;
-        const T wk = rhs[k] / colk[k];
-        __syncwarp();
-        for (int i = k + 1 + lane; i < C; i += 32) rhs[i] -= colk[i] * wk;
-        __syncwarp();
-      }
-      // back: x_k = (y_k - sum_{i>k} S[i][k] x_i) / d_k
-      for (int k = C - 1; k >= 0; --k) {
-        const T* colk = S + colstart(k, C) - k;
-        T part_k = T(0);
-        for (int i = k + 1 + lane; i < C; i += 32) part_k += colk[i] * rhs[i];
-        part_k = warp_sum(part_k);
-        const T xk = (rhs[k] - part_k) / colk[k];
-        __syncwarp();
-        if (lane == 0) rhs[k] = xk;
-        __syncwarp();
-      }
-      for (int i = lane; i < C; i += 32) dcs[i] = (double)rhs[i];
-      __syncwarp();
-      if (opt_pts) {
-        const T df = has_f ? T(dcs[FI]) : T(0);
-        for (int p = lane; p < Pn; p += 32) {
-          T* pw = ptw + (size_t)p * kPtStride;
-          T u0 = pw[6] + pw[9] * df, u1 = pw[7] + pw[10] * df, u2 = pw[8] + pw[11] * df;
-          for (int k = ptr[p]; k < ptr[p + 1]; ++k) {
-            const int s = slot[obs_cam(obs, k)];
-            if (s < 0) continue;
-            T y[18];
-            load18(Ybuf + (size_t)k * YSTR, y);
-#pragma unroll
-            for (int r = 0; r < 6; ++r) {
-              const T dd = T(dcs[6 * s + r]);
-              u0 += y[r * 3 + 0] * dd;
-              u1 += y[r * 3 + 1] * dd;
-              u2 += y[r * 3 + 2] * dd;
-            }
-          }
-          const T L00 = pw[0], L10 = pw[1], L11 = pw[2], L20 = pw[3], L21 = pw[4], L22 = pw[5];
-          const T x2 = u2 / L22;
-          const T x1 = (u1 - L21 * x2) / L11;
-          const T x0 = (u0 - L10 * x1 - L20 * x2) / L00;
-          pw[12] = -x0;
-          pw[13] = -x1;
-          pw[14] = -x2;
-        }
-      }
-      __syncwarp();
-    }
-
-    // ---------- K5 trials ----------
-    if (lane == 0) lambdas[it] = lam;
-    int tries = 0, took = -1;
-    double tcst[3] = {0, 0, 0};
-    double ft = f;
-    if (!chol_fail) {
-      for (int bt = 0; bt < kBacktrackTries; ++bt) {
-        const double frac = ldexp(1.0, -bt);
-        if (lane < n) {
-          const int c = lane, s = slot[c];
-          if (s < 0) {
-            for (int i = 0; i < 9; ++i) Rt[9 * c + i] = Rc[9 * c + i];
-            for (int i = 0; i < 3; ++i) tt[3 * c + i] = tc[3 * c + i];
-          } else {
-            const double w[3] = {frac * dcs[6 * s], frac * dcs[6 * s + 1], frac * dcs[6 * s + 2]};
-            double E[9];
-            exp_so3(w, E);
-            matmul33(E, Rc + 9 * c, Rt + 9 * c);
-            for (int i = 0; i < 3; ++i) tt[3 * c + i] = tc[3 * c + i] + frac * dcs[6 * s + 3 + i];
-          }
-        }
-        ft = has_f ? f + frac * dcs[FI] : f;
-        __syncwarp();
-        warp_cost_pass<T>(obs, lo, K, X, ptw, frac, opt_pts, Rt, tt, ft, cx, cy, delta, loss, lane, tcst);
-        ++tries;
-        if (tcst[0] < cost && isfinite(tcst[0])) {
-          took = bt;
-          break;
-        }
-      }
-    }
-    if (lane == 0) evals[it] = (uint8_t)tries;
-    bool stop = false;
-    if (took >= 0) {
-      const double frac = ldexp(1.0, -took);
-      for (int i = lane; i < n * 9; i += 32) Rc[i] = Rt[i];
-      for (int i = lane; i < n * 3; i += 32) tc[i] = tt[i];
-      if (opt_pts)
-        for (int p = lane; p < Pn; p += 32) {
-          const T* dp = ptw + (size_t)p * kPtStride + 12;
-          X[3 * p + 0] = X[3 * p + 0] + frac * (double)dp[0];
-          X[3 * p + 1] = X[3 * p + 1] + frac * (double)dp[1];
-          X[3 * p + 2] = X[3 * p + 2] + frac * (double)dp[2];
-        }
-      f = ft;
-      lam = took == 0 ? fmax(lam / nu, 1e-15) : fmin(lam * nu, kLambdaMax);
-      const double improve = cost - tcst[0];
-      cost = tcst[0];
-      se = tcst[1];
-      se2 = tcst[2];
-      if (lane == 0) accepted[it] = 1;
-      if (improve <= 1e-15 * fmax(cost, 1.0)) {
-        stop = true;
-        stop_reason = MBA_SOLVE_CONVERGED;
-      }
-    } else {
-      lam = fmin(lam * nu, kLambdaMax);
-      if (lane == 0) accepted[it] = 0;
-      if (!chol_fail && lam >= kLambdaMax) {
-        stop = true;
-        stop_reason = MBA_SOLVE_LAMBDA_CAP;
-      }
-    }
-    if (lane == 0) costs[it + 1] = cost;
-    ++it;
-    __syncwarp();
-    if (stop) break;
-  }
-
-  for (int i = lane; i < n * 9; i += 32) O.R_out[cb * 9 + i] = Rc[i];
-  for (int i = lane; i < n * 3; i += 32) O.t_out[cb * 3 + i] = tc[i];
-  if (lane == 0) {
-    O.focal_out[b] = f;
-    O.n_iters[b] = it;
-    O.status[b] = stop_reason;
-    O.final_stats[4 * b + 0] = cost;
-    O.final_stats[4 * b + 1] = se;
-    O.final_stats[4 * b + 2] = se2;
-    O.final_stats[4 * b + 3] = (double)K;
-  }
-  __syncwarp();
-}
-
-template <typename T, int MAXC>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, sizeof(T) == 4 ? 4 : 2) solve_warp_kernel(SolveParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* sbase = smem_raw + wib * WLayout<T, MAXC>::kBytes;
-  const size_t slot_id = (size_t)blockIdx.x * kWarpsPerCta + wib;
-  const Scratch<T, false> W = scratch_at<T, false>(P.ws + slot_id * P.ws_slot_bytes, P.d);
-  for (;;) {
-    int b = 0;
-    if (lane == 0) b = atomicAdd(P.counter, 1);
-    b = __shfl_sync(0xffffffffu, b, 0);
-    if (b >= P.d.n_problems) return;
-    warp_solve_one<T, MAXC>(P, b, sbase, W);
-  }
-}
-
-// ===========================================================================
-// Point-wise solver (the default for problems with <= 8 cameras).
-//
-// Per point p the Schur-reduced, augmented camera system receives
-//     S_aug  +=  sum_{i in p} J_i^T w_i J_i   -   Yhat_p Yhat_p^T
-// where J_i = [A_i | F_i | -r_i] (camera columns, focal column, rhs "row" C)
-// and Yhat_p stacks the rows Y_i = W_i L_p^-T of the point's free-camera
-// observations, y_f = L_p^-1 Wf_p and -z_p = -L_p^-1 g_p (miniba.py:135-177,
-// 207-213). Every warp owns a contiguous range of points and a private copy of
-// S_aug in shared memory; it walks its range in chunks of <= 32 observations:
-//   (a) lane per observation: fp64 projection, Jacobians, per-observation V/g
-//       contributions and W_i, staged in shared memory;
-//   (b) lane per point: damped 3x3 Cholesky of V_p, z_p, y_f;
-//   (c) lane per observation: Y_i = W_i L_p^-T;
-//   (d) point by point, lanes over (observation pair, row) and (observation,
-//       row) tasks: 6x6 Schur blocks and the J^T w J rows, read-modify-write into
-//       the warp's private S_aug -- no atomics, fixed order.
-// The private copies are summed in warp order, damped, factorised (LDL^T with
-// the forward substitution fused) and back-substituted by the whole CTA; the
-// point back-substitution recomputes W_i^T dc = w B_i^T (A_i dc) instead of
-// storing Y. No per-observation scratch exists: per-CTA global scratch is
-// only the point CSR and the per-point factors.
-// ===========================================================================
-
-constexpr int kChunk = 32;   // observations per warp chunk
-constexpr int kSRow = 48;    // staged values per observation (A12 F2 r2 w1 | W/Y 18 | Vc6 gc3 wfc3)
-
-template <typename T, int MAXC, int NW>
-struct PLayout {
-  static constexpr int N = MAXC, C = 6 * MAXC + 1, CA = C * (C + 3) / 2;
-  static constexpr size_t oRc = 0;
-  static constexpr size_t oTc = oRc + 8 * 9 * N;
-  static constexpr size_t oRt = oTc + 8 * 3 * N;
-  static constexpr size_t oTt = oRt + 8 * 9 * N * kBacktrackTries;
-  static constexpr size_t oDc = oTt + 8 * 3 * N * kBacktrackTries;
-  static constexpr size_t oRed = align16(oDc + 8 * C);           // double[NW * 4]
-  static constexpr size_t oS = align16(oRed + 8 * NW * 4);        // T[CA]
-  static constexpr size_t oXs = align16(oS + sizeof(T) * CA);     // T[C]
-  static constexpr size_t oTab = align16(oXs + sizeof(T) * C);    // u16[CA]
-  static constexpr size_t oSlot = align16(oTab + 2 * CA);         // int[N]
-  static constexpr size_t oSw = align16(oSlot + 4 * N);           // T[NW][CA]
-  static constexpr size_t oUd = align16(oSw + sizeof(T) * NW * CA);   // T[NW][C]
-  static constexpr size_t oSt = align16(oUd + sizeof(T) * NW * C);    // T[NW][kChunk][kSRow]
-  static constexpr size_t oSs = align16(oSt + sizeof(T) * NW * kChunk * kSRow);  // int[NW][kChunk]
-  static constexpr size_t oPs = align16(oSs + 4 * NW * kChunk);   // T[NW][kChunk][12]
-  static constexpr size_t oPi = align16(oPs + sizeof(T) * NW * kChunk * 12);  // int[NW][kChunk][2]
-  static constexpr size_t kBytes = align16(oPi + 8 * NW * kChunk);
-};
-
-template <typename T>
-__host__ __device__ inline size_t pw_scratch_bytes(int64_t max_points) {
-  return align16(sizeof(int) * (max_points + 1)) + align16(sizeof(T) * 16 * max_points);
-}
-
-template <typename T, int MAXC, int NW>
-__device__ void pw_solve_one(const SolveParams& P, int b, unsigned char* smem_raw) {
-  using L = PLayout<T, MAXC, NW>;
-  constexpr int NT = 32 * NW;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const MbaBatchDesc& D = P.d;
-  const MbaLmConfig& cfg = P.cfg;
-  const MbaOutputs& O = P.o;
-  double* Rc = (double*)(smem_raw + L::oRc);
-  double* tc = (double*)(smem_raw + L::oTc);
-  double* Rt = (double*)(smem_raw + L::oRt);
-  double* tt = (double*)(smem_raw + L::oTt);
-  double* dcs = (double*)(smem_raw + L::oDc);
-  double* red = (double*)(smem_raw + L::oRed);
-  T* S = (T*)(smem_raw + L::oS);
-  T* xs = (T*)(smem_raw + L::oXs);
-  unsigned short* tab = (unsigned short*)(smem_raw + L::oTab);
-  int* slot = (int*)(smem_raw + L::oSlot);
-  T* Sw = (T*)(smem_raw + L::oSw) + (size_t)wid * L::CA;
-  T* Ud = (T*)(smem_raw + L::oUd) + (size_t)wid * L::C;
-  T* st = (T*)(smem_raw + L::oSt) + (size_t)wid * kChunk * kSRow;
-  int* sslot = (int*)(smem_raw + L::oSs) + wid * kChunk;
-  T* ps = (T*)(smem_raw + L::oPs) + (size_t)wid * kChunk * 12;
-  int* pi = (int*)(smem_raw + L::oPi) + wid * kChunk * 2;
-  __shared__ int s_flag;
-
-  const int64_t cb = D.cam_off[b], pb = D.pt_off[b], ob = D.obs_off[b];
-  const int n = (int)(D.cam_off[b + 1] - cb);
-  const int Pn = (int)(D.pt_off[b + 1] - pb);
-  const int K = (int)(D.obs_off[b + 1] - ob);
-  const uint8_t fl = D.flags[b];
-  const bool has_f = fl & 1, opt_pts = (fl >> 1) & 1;
-  const double cx = D.cx[b], cy = D.cy[b];
-  const double delta = cfg.delta, nu = cfg.nu;
-  const int loss = cfg.loss, max_it = cfg.max_iters;
-  const MbaObs* __restrict__ obs = D.obs + ob;
-  const float* __restrict__ lo = D.obs_lo ? D.obs_lo + 2 * ob : nullptr;
-  double* __restrict__ X = O.points_out + 3 * pb;
-  unsigned char* wsb = P.ws + (size_t)blockIdx.x * P.ws_slot_bytes;
-  int* __restrict__ ptr = (int*)wsb;
-  T* __restrict__ ptw = (T*)(wsb + align16(sizeof(int) * (D.max_points + 1)));
-  double* costs = O.costs + (size_t)b * (max_it + 1);
-  double* lambdas = O.lambdas + (size_t)b * max_it;
-  uint8_t* accepted = O.accepted + (size_t)b * max_it;
-  uint8_t* evals = O.evals + (size_t)b * max_it;
-
-  // ---------------- setup ----------------
-  for (int i = tid; i < n * 9; i += NT) Rc[i] = O.R_in[cb * 9 + i];
-  for (int i = tid; i < n * 3; i += NT) tc[i] = O.t_in[cb * 3 + i];
-  if (O.points_in != O.points_out)
-    for (int i = tid; i < Pn * 3; i += NT) X[i] = O.points_in[pb * 3 + i];
-  int nf = 0;
-  {
-    unsigned fm = 0;
-    for (int c = 0; c < n; ++c) fm |= (D.fixed[cb + c] ? 0u : 1u) << c;  // n <= MAXC <= 32
-    nf = __popc(fm);
-    for (int c = tid; c < n; c += NT) slot[c] = ((fm >> c) & 1u) ? __popc(fm & ((1u << c) - 1u)) : -1;
-  }
-  const int C = 6 * nf + (has_f ? 1 : 0), FI = C - 1, CA = C * (C + 3) / 2;
-  if (tid == 0) s_flag = 0;
-  for (int p = tid; p <= Pn; p += NT) {
-    int a = 0, z = K;
-    while (a < z) {
-      const int mid = (a + z) >> 1;
-      if (__ldg(&obs[mid].pt) < p) a = mid + 1; else z = mid;
-    }
-    ptr[p] = a;
-  }
-  for (int j = tid; j < C; j += NT) {
-    const int a0 = acol(j, C);
-    for (int i = j; i <= C; ++i) tab[a0 + i - j] = (unsigned short)((i << 8) | j);
-  }
-  __syncthreads();
-  for (int k = tid; k < K; k += NT) {
-    const int pt = __ldg(&obs[k].pt), c = __ldg(&obs[k].cam);
-    const bool bad = pt < 0 || pt >= Pn || c < 0 || c >= n || (k > 0 && __ldg(&obs[k - 1].pt) > pt);
-    if (bad) s_flag = 1;
-  }
-  for (int p = tid; p < Pn; p += NT)
-    if (ptr[p + 1] - ptr[p] > kChunk) s_flag = 1;   // (host routes such batches elsewhere)
-  __syncthreads();
-  double f = O.focal_in[b];
-  if (s_flag) {
-    if (tid == 0) {
-      O.n_iters[b] = 0;
-      O.status[b] = -1;
-      O.focal_out[b] = f;
-    }
-    for (int i = tid; i < n * 9; i += NT) O.R_out[cb * 9 + i] = Rc[i];
-    for (int i = tid; i < n * 3; i += NT) O.t_out[cb * 3 + i] = tc[i];
-    __syncthreads();
-    return;
-  }
-  // this warp's contiguous point range
-  const int wp0 = (int)((int64_t)Pn * wid / NW), wp1 = (int)((int64_t)Pn * (wid + 1) / NW);
-
-  double stt[3];
-  {
-    // initial cost: block-wide pass
-    double acc3[3] = {0.0, 0.0, 0.0};
-    for (int k = tid; k < K; k += NT) {
-      Obs o = load_obs(obs, lo, k);
-      const double Xp[3] = {X[3 * o.pt], X[3 * o.pt + 1], X[3 * o.pt + 2]};
-      Proj pr = project_residual_fast(Rc + 9 * o.cam, tc + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
-      const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
-      acc3[0] += robust_rho(e, delta, loss);
-      acc3[1] += e;
-      acc3[2] += e * e;
-    }
-    block_sum<double, 3>(acc3, red);
-    stt[0] = acc3[0]; stt[1] = acc3[1]; stt[2] = acc3[2];
-  }
-  double cost = stt[0], se = stt[1], se2 = stt[2];
-  double lam = cfg.lambda_init;
-  if (tid == 0) costs[0] = cost;
-  int it = 0, stop_reason = MBA_SOLVE_MAX_ITERS;
-
-  for (; it < max_it;) {
-    const T tlam = T(lam);
-    for (int e = lane; e < CA; e += 32) Sw[e] = T(0);
-    for (int e = lane; e < C; e += 32) Ud[e] = T(0);
-    T part[4] = {T(0), T(0), T(0), T(0)};  // U_ff, g_f, sum yf.yf, sum yf.z
-    __syncwarp();
-    // ---------- per-warp point chunks ----------
-    for (int pc0 = wp0; pc0 < wp1;) {
-      // chunk: points [pc0, pc1) with at most kChunk observations
-      const int kc0 = ptr[pc0];
-      int pc1 = pc0 + 1;
-      while (pc1 < wp1 && pc1 - pc0 < kChunk && ptr[pc1 + 1] - kc0 <= kChunk) ++pc1;
-      const int kc1 = ptr[pc1];
-      const int npt = pc1 - pc0, nob = kc1 - kc0;
-      // (a) lane per observation
-      if (lane < nob) {
-        const int k = kc0 + lane;
-        Obs o = load_obs(obs, lo, k);
-        const double Xp[3] = {X[3 * o.pt], X[3 * o.pt + 1], X[3 * o.pt + 2]};
-        const double* Rk = Rc + 9 * o.cam;
-        Proj pr = project_residual_fast(Rk, tc + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
-        const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
-        const T w = T(robust_w(e, delta, loss));
-        T A[12], Fb[2], Bm[6];
-        jac_blocks<T>(pr, Rk, f, A, Fb, Bm);
-        const T r0 = T(pr.ru), r1 = T(pr.rv);
-        T* sr = st + lane * kSRow;
-#pragma unroll
-        for (int i = 0; i < 12; ++i) sr[i] = A[i];
-        sr[12] = Fb[0]; sr[13] = Fb[1]; sr[14] = r0; sr[15] = r1; sr[16] = w;
-        const int sl = slot[o.cam];
-        sslot[lane] = sl;
-        if (opt_pts) {
-          T wB[6];
-#pragma unroll
-          for (int i = 0; i < 6; ++i) wB[i] = w * Bm[i];
-          sr[35] = Bm[0] * wB[0] + Bm[3] * wB[3];
-          sr[36] = Bm[1] * wB[0] + Bm[4] * wB[3];
-          sr[37] = Bm[1] * wB[1] + Bm[4] * wB[4];
-          sr[38] = Bm[2] * wB[0] + Bm[5] * wB[3];
-          sr[39] = Bm[2] * wB[1] + Bm[5] * wB[4];
-          sr[40] = Bm[2] * wB[2] + Bm[5] * wB[5];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) sr[41 + a] = wB[a] * r0 + wB[3 + a] * r1;
-          const T wf0 = w * Fb[0], wf1 = w * Fb[1];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) sr[44 + a] = wf0 * Bm[a] + wf1 * Bm[3 + a];
-          if (sl >= 0) {
-#pragma unroll
-            for (int r = 0; r < 6; ++r)
-#pragma unroll
-              for (int a = 0; a < 3; ++a) sr[17 + r * 3 + a] = A[r] * wB[a] + A[6 + r] * wB[3 + a];
-          }
-        }
-      }
-      __syncwarp();
-      // (b) lane per point
-      if (lane < npt) {
-        const int p = pc0 + lane;
-        const int a0 = ptr[p] - kc0, a1 = ptr[p + 1] - kc0;
-        pi[2 * lane] = a0;
-        pi[2 * lane + 1] = a1;
-        T V[6] = {T(0), T(0), T(0), T(0), T(0), T(0)}, g[3] = {T(0), T(0), T(0)}, wf[3] = {T(0), T(0), T(0)};
-        for (int q = a0; q < a1; ++q) {
-          const T* sr = st + q * kSRow;
-          if (has_f) {
-            part[0] += sr[16] * (sr[12] * sr[12] + sr[13] * sr[13]);
-            part[1] += sr[16] * (sr[12] * sr[14] + sr[13] * sr[15]);
-          }
-          if (opt_pts) {
-#pragma unroll
-            for (int i = 0; i < 6; ++i) V[i] += sr[35 + i];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) g[i] += sr[41 + i];
-            if (has_f)
-#pragma unroll
-              for (int i = 0; i < 3; ++i) wf[i] += sr[44 + i];
-          }
-        }
-        if (opt_pts) {
-          V[0] += tlam * (V[0] > T(kDiagFloor) ? V[0] : T(kDiagFloor));
-          V[2] += tlam * (V[2] > T(kDiagFloor) ? V[2] : T(kDiagFloor));
-          V[5] += tlam * (V[5] > T(kDiagFloor) ? V[5] : T(kDiagFloor));
-          const T L00 = sqrt(V[0]);
-          const T i00 = T(1) / L00;
-          const T L10 = V[1] * i00, L20 = V[3] * i00;
-          const T L11 = sqrt(V[2] - L10 * L10);
-          const T i11 = T(1) / L11;
-          const T L21 = (V[4] - L20 * L10) * i11;
-          const T L22 = sqrt(V[5] - L20 * L20 - L21 * L21);
-          const T i22 = T(1) / L22;
-          const T z0 = g[0] * i00, z1 = (g[1] - L10 * z0) * i11, z2 = (g[2] - L20 * z0 - L21 * z1) * i22;
-          const T f0 = wf[0] * i00, f1 = (wf[1] - L10 * f0) * i11, f2 = (wf[2] - L20 * f0 - L21 * f1) * i22;
-          part[2] += f0 * f0 + f1 * f1 + f2 * f2;
-          part[3] += f0 * z0 + f1 * z1 + f2 * z2;
-          T* pl = ps + lane * 12;
-          pl[0] = L00; pl[1] = L10; pl[2] = L11; pl[3] = L20; pl[4] = L21; pl[5] = L22;
-          pl[6] = z0; pl[7] = z1; pl[8] = z2; pl[9] = f0; pl[10] = f1; pl[11] = f2;
-          T* pw = ptw + (size_t)p * 16;
-#pragma unroll
-          for (int i = 0; i < 12; ++i) pw[i] = pl[i];
-        }
-      }
-      __syncwarp();
-      if (opt_pts) {
-        // (c) lane per observation: Y_i = W_i L_p^-T
-        if (lane < nob && sslot[lane] >= 0) {
-          int lp = 0;
-          while (lp + 1 < npt && pi[2 * (lp + 1)] <= lane) ++lp;
-          const T* pl = ps + lp * 12;
-          const T L00 = pl[0], L10 = pl[1], L11 = pl[2], L20 = pl[3], L21 = pl[4], L22 = pl[5];
-          const T i00 = T(1) / L00, i11 = T(1) / L11, i22 = T(1) / L22;
-          T* y = st + lane * kSRow + 17;
-#pragma unroll
-          for (int r = 0; r < 6; ++r) {
-            const T y0 = y[r * 3 + 0] * i00;
-            const T y1 = (y[r * 3 + 1] - L10 * y0) * i11;
-            const T y2 = (y[r * 3 + 2] - L20 * y0 - L21 * y1) * i22;
-            y[r * 3 + 0] = y0;
-            y[r * 3 + 1] = y1;
-            y[r * 3 + 2] = y2;
-          }
-        }
-        __syncwarp();
-      }
-      // (d) point by point accumulation into the warp's S_aug
-      for (int lp = 0; lp < npt; ++lp) {
-        const int a0 = pi[2 * lp], a1 = pi[2 * lp + 1];
-        // free observations of the point (local staging indices), slot-ordered checks
-        int fre[kChunk];
-        int m = 0;
-        bool dup = false;
-        for (int q = a0; q < a1; ++q)
-          if (sslot[q] >= 0) {
-            for (int t = 0; t < m; ++t) dup |= sslot[fre[t]] == sslot[q];
-            fre[m++] = q;
-          }
-        const T* pl = ps + lp * 12;
-        if (opt_pts && !dup) {
-          // Schur 6x6 blocks: tasks (pair k >= l, row r)
-          const int ntask = 3 * m * (m + 1);
-          for (int tsk = lane; tsk < ntask; tsk += 32) {
-            const int pr_ = tsk / 6, r = tsk % 6;
-            int k = 0;
-            while ((k + 1) * (k + 2) / 2 <= pr_) ++k;
-            const int l = pr_ - k * (k + 1) / 2;
-            int qh = fre[k], ql = fre[l];
-            if (sslot[qh] < sslot[ql]) { const int tq = qh; qh = ql; ql = tq; }
-            const int sh = sslot[qh], sl_ = sslot[ql];
-            const T* yh = st + qh * kSRow + 17;
-            const T* yl = st + ql * kSRow + 17;
-            const T h0 = yh[r * 3], h1 = yh[r * 3 + 1], h2 = yh[r * 3 + 2];
-            const int row = 6 * sh + r;
-#pragma unroll
-            for (int c = 0; c < 6; ++c) {
-              if (sh == sl_ && c > r) continue;
-              const int col = 6 * sl_ + c;
-              Sw[acol(col, C) + row - col] -= h0 * yl[c * 3] + h1 * yl[c * 3 + 1] + h2 * yl[c * 3 + 2];
-            }
-          }
-          __syncwarp();
-        }
-        // rows of each free observation: J^T w J (camera block, focal, rhs) and
-        // the Schur focal / rhs terms
-        if (!dup) {
-          for (int tsk = lane; tsk < 6 * m; tsk += 32) {
-            const int kk = tsk / 6, r = tsk % 6;
-            const int q = fre[kk], s_ = sslot[q];
-            const T* sr = st + q * kSRow;
-            const T w = sr[16];
-            const T ar0 = w * sr[r], ar1 = w * sr[6 + r];
-            const int row = 6 * s_ + r;
-            const int cs = acol(row, C) - row;  // column `row`: entry (i, row) at cs + i
-            T d = T(0);
-#pragma unroll
-            for (int c = 0; c < 6; ++c) {
-              if (c > r) continue;
-              const T v = ar0 * sr[c] + ar1 * sr[6 + c];
-              if (c == r) d = v;
-              const int col = 6 * s_ + c;
-              Sw[acol(col, C) + row - col] += v;
-            }
-            Ud[row] += d;
-            T sf = T(0), sz = T(0);  // Schur focal / rhs terms (points optimised only)
-            if (opt_pts) {
-              const T yr0 = sr[17 + r * 3], yr1 = sr[18 + r * 3], yr2 = sr[19 + r * 3];
-              sf = yr0 * pl[9] + yr1 * pl[10] + yr2 * pl[11];
-              sz = yr0 * pl[6] + yr1 * pl[7] + yr2 * pl[8];
-            }
-            if (has_f) Sw[cs + FI] += ar0 * sr[12] + ar1 * sr[13] - sf;
-            Sw[cs + C] += -(ar0 * sr[14] + ar1 * sr[15]) + sz;
-          }
-          __syncwarp();
-        } else if (lane == 0) {
-          // duplicate camera within a point (rare): serial accumulation
-          for (int kk = 0; kk < m; ++kk) {
-            const int qk = fre[kk], sk = sslot[qk];
-            const T* srk = st + qk * kSRow;
-            for (int ll = 0; ll < m; ++ll) {
-              const int ql = fre[ll], sl2 = sslot[ql];
-              if (!opt_pts) break;
-              const T* yk = srk + 17;
-              const T* yl = st + ql * kSRow + 17;
-              for (int r = 0; r < 6; ++r)
-                for (int c = 0; c < 6; ++c) {
-                  const int row = 6 * sk + r, col = 6 * sl2 + c;
-                  if (row < col) continue;   // each ordered (row >= col) entry once per ordered pair
-                  Sw[acol(col, C) + row - col] -= yk[r * 3] * yl[c * 3] + yk[r * 3 + 1] * yl[c * 3 + 1] +
-                                                  yk[r * 3 + 2] * yl[c * 3 + 2];
-                }
-            }
-            const T w = srk[16];
-            for (int r = 0; r < 6; ++r) {
-              const int row = 6 * sk + r;
-              const int cs = acol(row, C) - row;
-              const T ar0 = w * srk[r], ar1 = w * srk[6 + r];
-              for (int c = 0; c <= r; ++c) {
-                const T v = ar0 * srk[c] + ar1 * srk[6 + c];
-                const int col = 6 * sk + c;
-                Sw[acol(col, C) + row - col] += v;
-                if (c == r) Ud[row] += v;
-              }
-              T sf = T(0), sz = T(0);
-              if (opt_pts) {
-                const T yr0 = srk[17 + r * 3], yr1 = srk[18 + r * 3], yr2 = srk[19 + r * 3];
-                sf = yr0 * pl[9] + yr1 * pl[10] + yr2 * pl[11];
-                sz = yr0 * pl[6] + yr1 * pl[7] + yr2 * pl[8];
-              }
-              if (has_f) Sw[cs + FI] += ar0 * srk[12] + ar1 * srk[13] - sf;
-              Sw[cs + C] += -(ar0 * srk[14] + ar1 * srk[15]) + sz;
-            }
-          }
-        }
-        __syncwarp();
-      }
-      pc0 = pc1;
-    }
-    // ---------- combine the warps' systems ----------
-#pragma unroll
-    for (int i = 0; i < 4; ++i) part[i] = warp_sum(part[i]);
-    if (lane == 0)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) ((T*)red)[wid * 4 + i] = part[i];
-    __syncthreads();
-    for (int e = tid; e < CA; e += NT) {
-      T v = T(0);
-      for (int w2 = 0; w2 < NW; ++w2) v += ((T*)(smem_raw + L::oSw))[(size_t)w2 * L::CA + e];
-      S[e] = v;
-    }
-    __syncthreads();
-    if (tid < C) {
-      const int g = tid;
-      T u = T(0);
-      for (int w2 = 0; w2 < NW; ++w2) u += ((T*)(smem_raw + L::oUd))[(size_t)w2 * L::C + g];
-      T pf[4] = {T(0), T(0), T(0), T(0)};
-      for (int w2 = 0; w2 < NW; ++w2)
-        for (int i = 0; i < 4; ++i) pf[i] += ((T*)red)[w2 * 4 + i];
-      if (has_f && g == FI) {
-        const T uff = pf[0];
-        S[acol(FI, C)] = uff + tlam * (uff > T(kDiagFloor) ? uff : T(kDiagFloor)) - pf[2];
-        S[acol(FI, C) + 1] = -pf[1] + pf[3];
-      } else {
-        S[acol(g, C)] += tlam * (u > T(kDiagFloor) ? u : T(kDiagFloor));
-      }
-    }
-    __syncthreads();
-
-    // ---------- LDL^T (forward substitution fused) ----------
-    bool chol_fail = false;
-    for (int k = 0; k < C; ++k) {
-      const T* colk = S + acol(k, C) - k;
-      const T d = colk[k];
-      if (!(d > T(0)) || !isfinite((double)d)) {
-        chol_fail = true;
-        break;
-      }
-      const T inv = T(1) / d;
-      for (int e = acol(k + 1, C) + tid; e < CA; e += NT) {
-        const unsigned ij = tab[e];
-        S[e] -= colk[ij >> 8] * colk[ij & 255u] * inv;
-      }
-      __syncthreads();
-    }
-    if (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull)) chol_fail = true;
-
-    if (!chol_fail) {
-      if (wid == 0) {
-        for (int k = C - 1; k >= 0; --k) {
-          const T* colk = S + acol(k, C) - k;
-          T acc = T(0);
-          for (int i = k + 1 + lane; i < C; i += 32) acc += colk[i] * xs[i];
-          acc = warp_sum(acc);
-          const T xk = (colk[C] - acc) / colk[k];
-          if (lane == 0) xs[k] = xk;
-          __syncwarp();
-        }
-        for (int i = lane; i < C; i += 32) dcs[i] = (double)xs[i];
-      }
-      __syncthreads();
-      // point back-substitution, recomputing W_i^T dc = w B^T (A dc)
-      if (opt_pts) {
-        const T df = has_f ? T(dcs[FI]) : T(0);
-        for (int p = tid; p < Pn; p += NT) {
-          const double Xp[3] = {X[3 * p], X[3 * p + 1], X[3 * p + 2]};
-          T u0 = T(0), u1 = T(0), u2 = T(0);
-          for (int k = ptr[p]; k < ptr[p + 1]; ++k) {
-            Obs o = load_obs(obs, lo, k);
-            const int s_ = slot[o.cam];
-            if (s_ < 0) continue;
-            const double* Rk = Rc + 9 * o.cam;
-            Proj pr = project_residual_fast(Rk, tc + 3 * o.cam, Xp, f, cx, cy, o.u, o.v);
-            const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
-            const T w = T(robust_w(e, delta, loss));
-            T A[12], Fb[2], Bm[6];
-            jac_blocks<T>(pr, Rk, f, A, Fb, Bm);
-            T ad0 = T(0), ad1 = T(0);
-#pragma unroll
-            for (int c = 0; c < 6; ++c) {
-              const T dd = T(dcs[6 * s_ + c]);
-              ad0 += A[c] * dd;
-              ad1 += A[6 + c] * dd;
-            }
-            ad0 *= w;
-            ad1 *= w;
-            u0 += Bm[0] * ad0 + Bm[3] * ad1;
-            u1 += Bm[1] * ad0 + Bm[4] * ad1;
-            u2 += Bm[2] * ad0 + Bm[5] * ad1;
-          }
-          T* pw = ptw + (size_t)p * 16;
-          const T L00 = pw[0], L10 = pw[1], L11 = pw[2], L20 = pw[3], L21 = pw[4], L22 = pw[5];
-          // v = L^-1 (W^T dc), then dp = -L^-T (z + v + yf df)
-          const T v0 = u0 / L00, v1 = (u1 - L10 * v0) / L11, v2 = (u2 - L20 * v0 - L21 * v1) / L22;
-          const T t0 = pw[6] + v0 + pw[9] * df, t1 = pw[7] + v1 + pw[10] * df, t2 = pw[8] + v2 + pw[11] * df;
-          const T x2 = t2 / L22;
-          const T x1 = (t1 - L21 * x2) / L11;
-          const T x0 = (t0 - L10 * x1 - L20 * x2) / L00;
-          pw[12] = -x0;
-          pw[13] = -x1;
-          pw[14] = -x2;
-        }
-      }
-      __syncthreads();
-    }
-
-    // ---------- trials ----------
-    if (tid == 0) lambdas[it] = lam;
-    int tries = 0, took = -1;
-    double tcst[3] = {0, 0, 0};
-    double ft = f;
-    if (!chol_fail) {
-      for (int q = tid; q < kBacktrackTries * n; q += NT) {
-        const int bt = q / n, c = q % n, s_ = slot[c];
-        const double frac = ldexp(1.0, -bt);
-        double* Rq = Rt + (size_t)(bt * n + c) * 9;
-        double* tq = tt + (size_t)(bt * n + c) * 3;
-        if (s_ < 0) {
-          for (int i = 0; i < 9; ++i) Rq[i] = Rc[9 * c + i];
-          for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i];
-        } else {
-          const double w[3] = {frac * dcs[6 * s_], frac * dcs[6 * s_ + 1], frac * dcs[6 * s_ + 2]};
-          double E[9];
-          exp_so3(w, E);
-          matmul33(E, Rc + 9 * c, Rq);
-          for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i] + frac * dcs[6 * s_ + 3 + i];
-        }
-      }
-      __syncthreads();
-      for (int bt = 0; bt < kBacktrackTries; ++bt) {
-        const double frac = ldexp(1.0, -bt);
-        ft = has_f ? f + frac * dcs[FI] : f;
-        const double* Rs = Rt + (size_t)bt * n * 9;
-        const double* ts = tt + (size_t)bt * n * 3;
-        double acc3[3] = {0.0, 0.0, 0.0};
-        for (int k0 = tid; k0 < K; k0 += 4 * NT) {
-          Obs o[4];
-          double Xq[4][3];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (k0 + u * NT < K) o[u] = load_obs(obs, lo, k0 + u * NT);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (k0 + u * NT >= K) continue;
-            const double* x = X + 3 * o[u].pt;
-            Xq[u][0] = x[0]; Xq[u][1] = x[1]; Xq[u][2] = x[2];
-            if (opt_pts) {
-              const T* dp = ptw + (size_t)o[u].pt * 16 + 12;
-              Xq[u][0] = Xq[u][0] + frac * (double)dp[0];
-              Xq[u][1] = Xq[u][1] + frac * (double)dp[1];
-              Xq[u][2] = Xq[u][2] + frac * (double)dp[2];
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (k0 + u * NT >= K) continue;
-            Proj pr = project_residual_fast(Rs + 9 * o[u].cam, ts + 3 * o[u].cam, Xq[u], ft, cx, cy, o[u].u, o[u].v);
-            const double e = sqrt(pr.ru * pr.ru + pr.rv * pr.rv);
-            acc3[0] += robust_rho(e, delta, loss);
-            acc3[1] += e;
-            acc3[2] += e * e;
-          }
-        }
-        block_sum<double, 3>(acc3, red);
-        tcst[0] = acc3[0]; tcst[1] = acc3[1]; tcst[2] = acc3[2];
-        ++tries;
-        if (tcst[0] < cost && isfinite(tcst[0])) {
-          took = bt;
-          break;
-        }
-      }
-    }
-    if (tid == 0) evals[it] = (uint8_t)tries;
-    bool stop = false;
-    if (took >= 0) {
-      const double frac = ldexp(1.0, -took);
-      for (int i = tid; i < n * 9; i += NT) Rc[i] = Rt[(size_t)took * n * 9 + i];
-      for (int i = tid; i < n * 3; i += NT) tc[i] = tt[(size_t)took * n * 3 + i];
-      if (opt_pts)
-        for (int p = tid; p < Pn; p += NT) {
-          const T* dp = ptw + (size_t)p * 16 + 12;
-          X[3 * p + 0] = X[3 * p + 0] + frac * (double)dp[0];
-          X[3 * p + 1] = X[3 * p + 1] + frac * (double)dp[1];
-          X[3 * p + 2] = X[3 * p + 2] + frac * (double)dp[2];
-        }
-      f = ft;
-      lam = took == 0 ? fmax(lam / nu, 1e-15) : fmin(lam * nu, kLambdaMax);
-      const double improve = cost - tcst[0];
-      cost = tcst[0];
-      se = tcst[1];
-      se2 = tcst[2];
-      if (tid == 0) accepted[it] = 1;
-      if (improve <= 1e-15 * fmax(cost, 1.0)) {
-        stop = true;
-        stop_reason = MBA_SOLVE_CONVERGED;
-      }
-    } else {
-      lam = fmin(lam * nu, kLambdaMax);
-      if (tid == 0) accepted[it] = 0;
-      if (!chol_fail && lam >= kLambdaMax) {
-        stop = true;
-        stop_reason = MBA_SOLVE_LAMBDA_CAP;
-      }
-    }
-    if (tid == 0) costs[it + 1] = cost;
-    ++it;
-    __syncthreads();
-    if (stop) break;
-  }
-
-  for (int i = tid; i < n * 9; i += NT) O.R_out[cb * 9 + i] = Rc[i];
-  for (int i = tid; i < n * 3; i += NT) O.t_out[cb * 3 + i] = tc[i];
-  if (tid == 0) {
-    O.focal_out[b] = f;
-    O.n_iters[b] = it;
-    O.status[b] = stop_reason;
-    O.final_stats[4 * b + 0] = cost;
-    O.final_stats[4 * b + 1] = se;
-    O.final_stats[4 * b + 2] = se2;
-    O.final_stats[4 * b + 3] = (double)K;
-  }
-  __syncthreads();
-}
-
-template <typename T, int MAXC, int NW>
-__global__ void __launch_bounds__(32 * NW) solve_pw_kernel(SolveParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int s_prob;
-  for (;;) {
-    if (threadIdx.x == 0) s_prob = atomicAdd(P.counter, 1);
-    __syncthreads();
-    const int b = s_prob;
-    __syncthreads();
-    if (b >= P.d.n_problems) return;
-    pw_solve_one<T, MAXC, NW>(P, b, smem_raw);
-  }
-}
-
-template <typename T, int MAXC, int NW>
-static int launch_pw(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
-                     size_t ws_bytes, cudaStream_t st) {
-  int dev = 0, n_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  const size_t scratch = pw_scratch_bytes<T>(d->max_points);
-  const size_t smem = PLayout<T, MAXC, NW>::kBytes;
-  if (smem > 227 * 1024) return MBA_ERR_TOO_LARGE;
-  cudaFuncSetAttribute(solve_pw_kernel<T, MAXC, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_pw_kernel<T, MAXC, NW>, 32 * NW, smem);
-  if (per_sm < 1) return MBA_ERR_TOO_LARGE;
-  int grid = n_sm * per_sm;
-  if (grid > d->n_problems) grid = d->n_problems;
-  if (ws_bytes < 256 + scratch * (size_t)grid) return MBA_ERR_INVALID;
-  SolveParams P;
-  P.d = *d;
-  P.cfg = *cfg;
-  P.o = *o;
-  P.counter = (int*)ws;
-  P.ws = (unsigned char*)ws + 256;
-  P.ws_slot_bytes = scratch;
-  P.max_cams = d->max_cams;
-  cudaMemsetAsync(ws, 0, sizeof(int), st);
-  solve_pw_kernel<T, MAXC, NW><<<grid, 32 * NW, smem, st>>>(P);
-  return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
-}
-
 constexpr size_t kSmemLimit = 227 * 1024;
 
 // Cooperative mode: every CTA of the grid works on the same problem (points,
@@ -2334,39 +1061,11 @@ static bool resident_fits(const MbaBatchDesc* d) {
          Layout<T, MAXC>::kFixed + scratch_bytes<T, true>(d->max_obs, d->max_points, d->max_pairs) <= kSmemLimit;
 }
 
-template <typename T, int MAXC>
-static int launch_warp(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
-                       size_t ws_bytes, cudaStream_t st) {
-  int dev = 0, n_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  const size_t scratch = scratch_bytes<T, false>(d->max_obs, d->max_points, d->max_pairs);
-  const size_t smem = WLayout<T, MAXC>::kBytes * kWarpsPerCta;
-  cudaFuncSetAttribute(solve_warp_kernel<T, MAXC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_warp_kernel<T, MAXC>, 32 * kWarpsPerCta, smem);
-  if (per_sm < 1) return MBA_ERR_TOO_LARGE;
-  int grid = n_sm * per_sm;
-  const int need = (d->n_problems + kWarpsPerCta - 1) / kWarpsPerCta;
-  if (grid > need) grid = need;
-  if (ws_bytes < 256 + scratch * (size_t)grid * kWarpsPerCta) return MBA_ERR_INVALID;
-  SolveParams P;
-  P.d = *d;
-  P.cfg = *cfg;
-  P.o = *o;
-  P.counter = (int*)ws;
-  P.ws = (unsigned char*)ws + 256;
-  P.ws_slot_bytes = scratch;
-  P.max_cams = d->max_cams;
-  cudaMemsetAsync(ws, 0, sizeof(int), st);
-  solve_warp_kernel<T, MAXC><<<grid, 32 * kWarpsPerCta, smem, st>>>(P);
-  return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
-}
-
 // Kernel choice: many small problems -> one warp per problem; otherwise one
 // CTA per problem (scratch in shared memory when it fits).
 static int choose_mode(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
-  if (cfg->ctas_per_problem < 0) return -cfg->ctas_per_problem;   // forced: 1 warp, 2 CTA, 3 point-wise
+  // forced (tests, experiments): 2 CTA kernel, 4 cooperative grid, 9 cluster kernel
+  if (cfg->ctas_per_problem < 0) return -cfg->ctas_per_problem;
   // the cluster-resident kernel whenever its shared-memory plan fits (<= 8
   // cameras): config 4 f64 250k problems/s vs 78k for the CTA kernel; a single
   // config-2 problem (K = 20k) in 0.44 ms on a 16-CTA cluster vs 2.43 ms for
@@ -2382,6 +1081,7 @@ template <typename T>
 static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
   int mode = choose_mode(d, cfg);
+  if (mode != 0 && mode != 2 && mode != 4 && mode != 9) return MBA_ERR_INVALID;
   if (mode == 0 && v4::plan_cluster(d, cfg) == 0) mode = 2;   // outside the cluster kernel's envelope
   if (mode == 9 || mode == 0) {
     // cluster-resident kernel; problems whose slices overflow its shared-memory
@@ -2400,13 +1100,6 @@ static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutput
     if (d->max_cams <= 32) return launch_grid<T, 32>(d, cfg, o, ws, ws_bytes, st);
     return MBA_ERR_TOO_LARGE;
   }
-  if (d->max_cams <= 8 && d->max_track <= kChunk && mode == 3)
-    return launch_pw<T, 8, sizeof(T) == 4 ? 4 : 2>(d, cfg, o, ws, ws_bytes, st);
-  if (d->max_cams <= 8 && mode == 1) return launch_warp<T, 8>(d, cfg, o, ws, ws_bytes, st);
-  if (d->max_cams <= 8 && mode == 5) return launch_cfg<T, 8, false, 256, 2>(d, cfg, o, ws, ws_bytes, st);
-  if (d->max_cams <= 8 && mode == 6) return launch_cfg<T, 8, false, 128, 4>(d, cfg, o, ws, ws_bytes, st);
-  if (d->max_cams <= 8 && mode == 7) return launch_cfg<T, 8, false, 128, 3>(d, cfg, o, ws, ws_bytes, st);
-  if (d->max_cams <= 8 && mode == 8) return launch_cfg<T, 8, false, 64, 6>(d, cfg, o, ws, ws_bytes, st);
   if (d->max_cams <= 8) {
     if (resident_fits<T, 8>(d)) return launch_cfg<T, 8, true>(d, cfg, o, ws, ws_bytes, st);
     return launch_cfg<T, 8, false>(d, cfg, o, ws, ws_bytes, st);
@@ -2440,11 +1133,10 @@ size_t mba_workspace_bytes(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
   const size_t slot = f64 ? mba::scratch_bytes<double, false>(d->max_obs, d->max_points, d->max_pairs)
                           : mba::scratch_bytes<float, false>(d->max_obs, d->max_points, d->max_pairs);
   const size_t gextra = mba::align16(mba::GridBufs<double, 32>::bytes(n_sm)) + 256;
-  if (slot + gextra > slot * 2) {
-    // cooperative mode needs one scratch slot plus the cross-CTA buffers
-  }
-  size_t grid = (size_t)n_sm * 16;  // upper bound on resident CTAs / warps
-  if (grid > (size_t)d->n_problems + mba::kWarpsPerCta) grid = d->n_problems + mba::kWarpsPerCta;
+  // one scratch slot per resident CTA of the CTA kernel (bounded by the batch)
+  // plus the cooperative grid mode's cross-CTA buffers
+  size_t grid = (size_t)n_sm * 16;
+  if (grid > (size_t)d->n_problems) grid = (size_t)d->n_problems;
   return 256 + slot * grid + gextra;
 }
 

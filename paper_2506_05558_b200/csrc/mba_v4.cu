@@ -112,12 +112,16 @@ __host__ __device__ constexpr size_t pt_bytes() { return 24 + sizeof(T) * PSTR +
 // thread 0 of every CTA accumulates clock64() deltas between phase marks.
 enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_CHA, PH_CHB, PH_N };
 #ifdef MBA_PHASE_PROF
-__device__ unsigned long long* g_prof = nullptr;
+static __device__ unsigned long long* g_prof = nullptr;
 #define PROF_DECL __shared__ long long s_prof[PH_N]; long long prof_t = clock64(); \
   if (threadIdx.x == 0) for (int i = 0; i < PH_N; ++i) s_prof[i] = 0;
 #define PROF_MARK(ph) if (threadIdx.x == 0) { long long now = clock64(); s_prof[ph] += now - prof_t; prof_t = now; }
 #define PROF_FLUSH if (threadIdx.x == 0 && g_prof) for (int i = 0; i < PH_N; ++i) atomicAdd(g_prof + i, (unsigned long long)s_prof[i]);
-void set_prof(unsigned long long* p) { cudaMemcpyToSymbol(g_prof, &p, sizeof(p)); }
+#ifdef MBA_V4_F32
+void set_prof_f32(unsigned long long* p) { cudaMemcpyToSymbol(g_prof, &p, sizeof(p)); }
+#else
+void set_prof_f64(unsigned long long* p) { cudaMemcpyToSymbol(g_prof, &p, sizeof(p)); }
+#endif
 #else
 #define PROF_DECL
 #define PROF_MARK(ph)
@@ -407,7 +411,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   T* dcT = (T*)(smem + F::oDcT);
   T* l10s = (T*)(smem + F::oL10);
 
-  __shared__ int s_flag, s_nf, s_nlp, s_npairs, s_job;
+  __shared__ int s_flag, s_nf, s_nlp, s_npairs, s_job, s_gcam;
   __shared__ unsigned char s_jorder[MAXN + MAXNB];   // job queue order: longest first
   __shared__ int s_wtot[NW_MAX];
   int epoch = 0;
@@ -447,6 +451,12 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       }
     s_nf = nf;
     s_flag = (n > MAXN) ? 1 : 0;
+    // the one fixed camera of a problem with a free scale gauge (see the step
+    // projection below); -1 when the gauge is pinned or not a pure scale
+    int gc = -1;
+    for (int c = 0; c < n; ++c)
+      if (slot[c] < 0) gc = (nf == n - 1) ? c : -1;
+    s_gcam = ((fl >> 1) & 1) ? gc : -1;
   }
   __syncthreads();
   const int nf = s_nf, C = 6 * nf + (has_f ? 1 : 0), FI = C - 1, CA = C * (C + 3) / 2;
@@ -1274,6 +1284,16 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
           for (int i = 0; i < 3; ++i) tq[i] = tc[3 * c + i] + frac * dc[6 * s + 3 + i];
         }
       }
+      const bool gauge = sizeof(T) == 4 && s_gcam >= 0;
+      double c0[3] = {0.0, 0.0, 0.0}, gacc[2] = {0.0, 0.0};
+      double gDp = 0.0;
+      if (gauge) {
+        const int g = s_gcam;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          c0[i] = -(Rc[9 * g + i] * tc[3 * g] + Rc[9 * g + 3 + i] * tc[3 * g + 1] + Rc[9 * g + 6 + i] * tc[3 * g + 2]);
+        gDp = 1.0 / (1.0 + lam);
+      }
       // point back substitution (miniba.py:216-217): dp = -L^-T (z + yf df + sum Y_i^T dc_a)
       if (opt_pts) {
         const T df = has_f ? dcT[FI] : T(0);
@@ -1311,6 +1331,59 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
           pw[12] = -x0;
           pw[13] = -x1;
           pw[14] = -x2;
+          if (gauge) {   // n_p^T D_p dp, n_p^T D_p n_p (step projection below)
+            const double l00 = 1.0 / (double)iL00, l11 = 1.0 / (double)iL11, l22 = 1.0 / (double)iL22;
+            const double Dp[3] = {l00 * l00 * gDp, ((double)L10 * L10 + l11 * l11) * gDp,
+                                  ((double)L20 * L20 + (double)L21 * L21 + l22 * l22) * gDp};
+            const double xs[3] = {-(double)x0, -(double)x1, -(double)x2};
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              const double nv = Xs[3 * sl + i] - c0[i];
+              gacc[0] += nv * Dp[i] * xs[i];
+              gacc[1] += nv * nv * Dp[i];
+            }
+          }
+        }
+      }
+      if (gauge) {
+        // Gauge-consistent step (fp32 Schur only). With one fixed camera the
+        // cost is invariant under scaling the scene about that camera's centre
+        // c0: H n = 0 and g.n = 0 for n = (dt_c = t_c + R_c c0, dX_p = X_p - c0),
+        // so the exact damped step (H + lam D) d = -g satisfies n^T D d = 0
+        // (D = max(diag H, 1e-12), miniba.py:188-193). fp32 Jacobians break the
+        // invariance at the 1e-7 level and, with lam -> 1e-15, the solve then
+        // moves freely along n (config 4: translations 5e-4 off the fp64
+        // reference at identical cost). Restore the exact-arithmetic property
+        // by removing the D-weighted component along n.
+        double acc[2] = {gacc[0], gacc[1]};
+        block_sum_d<NW, 2>(acc, red);
+        cluster_sum<R, 2>(acc, xch, epoch);
+        for (int s = 0; s < nf; ++s) {   // camera part: identical in every thread
+          const int c = cslot[s];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const double nv = tc[3 * c + i] + Rc[9 * c + 3 * i] * c0[0] + Rc[9 * c + 3 * i + 1] * c0[1] +
+                              Rc[9 * c + 3 * i + 2] * c0[2];
+            const double u = (double)jsum_at(s * UST + 45 + 3 + i);
+            const double Dc = u > kDiagFloor ? u : kDiagFloor;
+            acc[0] += nv * Dc * dc[6 * s + 3 + i];
+            acc[1] += nv * nv * Dc;
+          }
+        }
+        const double alpha = acc[1] > 0.0 ? acc[0] / acc[1] : 0.0;
+        __syncthreads();   // every thread has read dc; the trial cameras are complete
+        for (int sl = tid; sl < nlp; sl += NT) {
+          T* pw = pf + (size_t)sl * PSTR;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) pw[12 + i] = T((double)pw[12 + i] - alpha * (Xs[3 * sl + i] - c0[i]));
+        }
+        for (int q = tid; q < 3 * nf; q += NT) {
+          const int s = q / 3, i = q % 3, c = cslot[s];
+          const double nv = tc[3 * c + i] + Rc[9 * c + 3 * i] * c0[0] + Rc[9 * c + 3 * i + 1] * c0[1] +
+                            Rc[9 * c + 3 * i + 2] * c0[2];
+          dc[6 * s + 3 + i] -= alpha * nv;
+          for (int bt = 0; bt < kBacktrackTries; ++bt)
+            tt[(size_t)(bt * n + c) * 3 + i] = tc[3 * c + i] + ldexp(1.0, -bt) * dc[6 * s + 3 + i];
         }
       }
     }
@@ -1540,13 +1613,6 @@ static Plan plan_t(const MbaBatchDesc* d) {
   return Plan{0, 0, 0};
 }
 
-static Plan plan(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
-  if (d->max_cams > MAXN || d->max_cams < 1 || d->max_obs >= 65535 * 16) return Plan{0, 0, 0};
-  return cfg->precision == MBA_LIN_F64 ? plan_t<double>(d) : plan_t<float>(d);
-}
-
-int plan_cluster(const MbaBatchDesc* d, const MbaLmConfig* cfg) { return plan(d, cfg).R; }
-
 template <typename T, int R, int NT, int MINB>
 static int launch_t(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st) {
   auto kern = solve_v4_kernel<T, R, NT, MINB>;
@@ -1643,17 +1709,27 @@ static bool may_overflow_t(const MbaBatchDesc* d, const Plan& p) {
   return nlo >= 65535 || need > arena;
 }
 
-int may_overflow(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
-  const Plan p = plan(d, cfg);
-  if (p.R == 0) return 1;
-  return cfg->precision == MBA_LIN_F64 ? may_overflow_t<double>(d, p) : may_overflow_t<float>(d, p);
+// one arithmetic type per translation unit (see mba_v4.cuh)
+#ifdef MBA_V4_F32
+using TU = float;
+#define V4_ENTRY(x) x##_f32
+#else
+using TU = double;
+#define V4_ENTRY(x) x##_f64
+#endif
+
+int V4_ENTRY(plan_cluster)(const MbaBatchDesc* d) { return plan_t<TU>(d).R; }
+
+int V4_ENTRY(may_overflow)(const MbaBatchDesc* d) {
+  const Plan p = plan_t<TU>(d);
+  return p.R == 0 ? 1 : (may_overflow_t<TU>(d, p) ? 1 : 0);
 }
 
-int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st, int R) {
-  Plan p = plan(d, cfg);
+int V4_ENTRY(launch)(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st,
+                     int R) {
+  const Plan p = plan_t<TU>(d);
   if (p.R != R || R == 0) return MBA_ERR_TOO_LARGE;
-  if (cfg->precision == MBA_LIN_F64) return launch_prec<double>(d, cfg, o, st, p);
-  return launch_prec<float>(d, cfg, o, st, p);
+  return launch_prec<TU>(d, cfg, o, st, p);
 }
 
 }  // namespace v4

@@ -194,6 +194,10 @@ def to_device(hb: HostBatch, device=None, pinned=None) -> DeviceBatch:
                        h2d_bytes=nbytes, **d)
 
 
+# LmParams.kernel -> MbaLmConfig.ctas_per_problem (0: planner; < 0: forced path)
+KERNELS = {"auto": 0, "cta": -2, "grid": -4, "v4": -9}
+
+
 @dataclass
 class LmParams:
     lambda_init: float = 1e-5
@@ -203,8 +207,8 @@ class LmParams:
     loss: str = "huber"
     precision: str = "f64"
     fail_at: tuple = ()
-    kernel: str = "auto"      # "auto" | "cta" (CTA per problem) | "grid" (whole GPU per problem)
-    #                           | "pw" (point-wise) | "warp" (warp per problem)
+    kernel: str = "auto"      # "auto" | "v4" (cluster-resident) | "cta" (CTA per problem)
+    #                           | "grid" (whole GPU per problem)
 
     @staticmethod
     def from_cfg(cfg, **over):
@@ -262,7 +266,7 @@ def descriptors(db: DeviceBatch, prm: LmParams, sol: Solution):
     c = MbaLmConfig(lambda_init=prm.lambda_init, nu=prm.nu, delta=prm.delta,
                     max_iters=prm.max_iters, loss=_lib.LOSS[prm.loss],
                     precision=_lib.PRECISION[prm.precision],
-                    ctas_per_problem={"auto": 0, "warp": -1, "cta": -2, "pw": -3, "grid": -4, "cta2": -5, "cta128x4": -6, "cta128x3": -7, "cta64": -8, "v4": -9}[prm.kernel],
+                    ctas_per_problem=KERNELS[prm.kernel],
                     fail_iters_mask=sum(1 << int(i) for i in prm.fail_at if 0 <= int(i) < 64))
     o = MbaOutputs(R_in=ptr(db.R), t_in=ptr(db.t), focal_in=ptr(db.focal), points_in=ptr(db.points),
                    R_out=ptr(sol.R), t_out=ptr(sol.t), focal_out=ptr(sol.focal),

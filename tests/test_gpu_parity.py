@@ -12,58 +12,33 @@ from oracle import miniba_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "grid", "v4"])
+@pytest.mark.parametrize("kernel", ["cta", "grid", "v4"])
 @pytest.mark.parametrize("path", golden_cases(), ids=golden_ids())
 def test_solver_matches_reference_golden(path, kernel, cuda_ok):
     """float64 mode (the API default): exact trace parity through i* (fp64
     rule) and the BASELINE final-value tolerances on every golden case, for
-    both the CTA-per-problem and the warp-per-problem kernel."""
+    the cluster-resident, CTA-per-problem and whole-GPU kernels."""
     prob, cfg, out = load_case(path)
     dev = run_device([prob], cfg, "f64", kernel=kernel)[0]
     assert_parity(dev, out["costs"], out["accepted"], out["evals"], out["lambdas"], out["R"],
                   out["t"], float(out["focal"]), label=f"{path}:f64")
 
 
-# Mixed precision (fp32 linearise/Schur/LDL^T): known, documented departures.
-# the smoke scenes have a free scale gauge (one fixed camera, free focal): fp32
-# steps drift along it, so raw translations differ ~1% while the cost agrees
-# to 1e-15; outliers20 flips accept decisions that are fp32 near-ties.
-MIXED_GAUGE_CASES = {"smoke_noisy", "smoke_noisefree"}
-MIXED_TRACE_EXEMPT = {"smoke_noisy", "outliers20"}
-
-
 @pytest.mark.parametrize("path", golden_cases(), ids=golden_ids())
 def test_mixed_precision_against_golden(path, cuda_ok):
+    """Mixed precision (fp32 linearise/Schur/LDL^T, fp64 state and cost) on
+    the cluster-resident kernel, held to the SAME rule as f64: traces identical
+    through the fp64 plateau index, BASELINE final tolerances on raw R, t, f.
+    (The gauge-consistent step projection in mba_v4.cu is what keeps fp32
+    Jacobians from drifting along the free scale gauge of one-fixed-camera
+    problems.)"""
     prob, cfg, out = load_case(path)
-    name = path.split("lm_")[-1][:-4]
-    dev = run_device([prob], cfg, "mixed")[0]
-    c_ref = out["costs"][-1]
-    assert abs(dev["costs"][-1] - c_ref) <= 1e-4 * abs(c_ref) + 1e-12
-    if name not in MIXED_TRACE_EXEMPT:
-        K = len(prob["uv"])
-        i_star = O.plateau_index(out["costs"], tau=1e-5, kappa=1e-8 * K)
-        np.testing.assert_array_equal(dev["accepted"][:i_star + 1], out["accepted"][:i_star + 1])
-        np.testing.assert_array_equal(dev["evals"][:i_star + 1], out["evals"][:i_star + 1])
-    R, t = dev["R"], dev["t"]
-    if name == "outliers20":
-        return  # fp32 accept flips on near-ties move the solution within the cost tolerance
-    if name in MIXED_GAUGE_CASES:
-        # compare modulo the free similarity gauge, as smoke_miniba.py:68-76 does
-        from gsrecon.scene import umeyama
-        ce = -np.einsum("nji,nj->ni", R, t)
-        cr = -np.einsum("nji,nj->ni", out["R"], out["t"])
-        s, Rg, tg = umeyama(ce, cr, with_scale=True)
-        aligned = s * ce @ Rg.T + tg
-        span = np.linalg.norm(cr.max(0) - cr.min(0))
-        assert np.abs(aligned - cr).max() <= 1e-4 * span
-    else:
-        for c in range(len(R)):
-            assert rot_err(R[c], out["R"][c]) <= 1e-3
-        scale = np.linalg.norm(out["t"], axis=1).max()
-        assert np.abs(t - out["t"]).max() <= 1e-3 * scale
+    dev = run_device([prob], cfg, "mixed", kernel="v4")[0]
+    assert_parity(dev, out["costs"], out["accepted"], out["evals"], out["lambdas"], out["R"],
+                  out["t"], float(out["focal"]), label=f"{path}:mixed")
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "v4"])
+@pytest.mark.parametrize("kernel", ["cta", "v4"])
 @pytest.mark.parametrize("precision", ["mixed", "f64"])
 def test_batched_matches_oracle_and_is_shard_invariant(precision, kernel, cuda_ok):
     from paper_2506_05558_b200.synth import make_batch
@@ -124,7 +99,7 @@ def test_cauchy_outliers_many_cameras(kernel, cuda_ok):
                   p["focal"], label="cauchy16")
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "grid", "v4"])
+@pytest.mark.parametrize("kernel", ["cta", "grid", "v4"])
 def test_fault_injection_matches_oracle(kernel, cuda_ok):
     from paper_2506_05558_b200.synth import make_batch
     p = make_batch(1, n_cams=8, K=2000, seed=4).problem(0)
@@ -149,7 +124,7 @@ def test_max_iters_zero_and_one(cuda_ok):
     np.testing.assert_allclose(d1["costs"], ref["costs"], rtol=1e-9)
 
 
-@pytest.mark.parametrize("kernel", ["cta", "warp", "pw", "v4"])
+@pytest.mark.parametrize("kernel", ["cta", "v4"])
 def test_all_cameras_fixed_focal_only(kernel, cuda_ok):
     """C = 1 (focal only) edge shape."""
     from paper_2506_05558_b200.synth import make_batch
@@ -161,7 +136,7 @@ def test_all_cameras_fixed_focal_only(kernel, cuda_ok):
     assert dev["accepted"][:3].tolist() == ref["accepted"][:3].tolist()
 
 
-@pytest.mark.parametrize("other", ["warp", "pw", "grid", "v4"])
+@pytest.mark.parametrize("other", ["grid", "v4"])
 def test_kernels_agree(other, cuda_ok):
     """All kernels implement the same arithmetic per problem up to reduction
     order: traces agree through i* and final costs to 1e-9 on 64 problems."""
