@@ -114,6 +114,22 @@ typedef struct {
   double* final_stats;       /* [n_problems][4]: cost, sum e, sum e^2, K         */
 } MbaOutputs;
 
+/* Device-side packing of raw per-problem observation arrays (BaProblem
+ * cam_idx / pt_idx / uv, miniba.py:65-83, uploaded as int32 / int32 / float64
+ * back to back per problem) into the MbaObs records mba_solve consumes:
+ * stable point-major order within each problem (numpy argsort(kind="stable")
+ * of pt_idx), u/v rounded to float, and -- when out_lo is not NULL -- the
+ * low-order float2 stream uv - float(uv). Replaces the host-side sort of the
+ * producers' track-major (miniba.py:762-770) or camera-major
+ * (smoke_miniba.py:50-55) arrays. Problems with an out-of-range index are
+ * written unsorted; mba_solve then reports them malformed (status -1).
+ * workspace: >= mba_pack_obs_workspace_bytes(total points) bytes. */
+size_t mba_pack_obs_workspace_bytes(int64_t total_points);
+int32_t mba_pack_obs(int32_t n_problems, const int64_t* obs_off, const int64_t* pt_off,
+                     const int64_t* cam_off, const int32_t* cam, const int32_t* pt, const double* uv,
+                     MbaObs* out, float* out_lo, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
 int32_t mba_abi_version(void);
 
 /* Bytes of device workspace mba_solve needs for this batch and config. */

@@ -85,6 +85,10 @@ def lib():
     L.mba_pose_lm.restype = i32
     L.mba_pose_lm.argtypes = [i32, i32, _vp, _vp, d, d, d, i32, d, d, d, _vp, _vp, _vp, i32, _vp,
                               _vp, d, _vp, _vp, _vp]
+    L.mba_pack_obs_workspace_bytes.restype = sz
+    L.mba_pack_obs_workspace_bytes.argtypes = [i64]
+    L.mba_pack_obs.restype = i32
+    L.mba_pack_obs.argtypes = [i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, sz, _vp]
     if L.mba_abi_version() != 1:
         raise RuntimeError("libminiba ABI version mismatch")
     _lib = L
@@ -93,7 +97,8 @@ def lib():
 
 EXPORTED = ("mba_abi_version", "mba_workspace_bytes", "mba_solve", "mba_solve_plan", "mba_solve_launches", "mba_residuals", "mba_robust",
             "mba_blocks", "mba_assemble", "mba_solve_step_scratch_bytes", "mba_solve_step",
-            "mba_pose_lm", "mba_triangulate", "mba_match_pairs")
+            "mba_pose_lm", "mba_triangulate", "mba_match_pairs", "mba_pack_obs_workspace_bytes",
+            "mba_pack_obs")
 
 
 def check(rc, what):

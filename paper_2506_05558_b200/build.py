@@ -14,7 +14,8 @@ LIB_PROF = os.path.join(HERE, "libminiba_prof.so")
 SOURCES = [("mba_solve.cu", [], "mba_solve.o"), ("mba_v4.cu", [], "mba_v4_f64.o"),
            ("mba_v4.cu", ["-DMBA_V4_F32"], "mba_v4_f32.o"), ("mba_stages.cu", [], "mba_stages.o"),
            ("mba_pose.cu", [], "mba_pose.o"), ("mba_tri.cu", [], "mba_tri.o"),
-           ("mba_match.cu", [], "mba_match.o")]
+           ("mba_match.cu", [], "mba_match.o"),
+           ("mba_pack.cu", [], "mba_pack.o")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -32,6 +33,8 @@ def _stale():
 def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str:
     """Compile libminiba.so (or libminiba_prof.so with per-phase cycle counters)."""
     lib = LIB_PROF if prof else LIB
+    if not prof:
+        build_host(force)
     if not force and not prof and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
@@ -66,5 +69,35 @@ def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str
     return lib
 
 
+HOST_SRC = os.path.join(CSRC, "host", "mba_host.cpp")
+
+
+def host_ext_path():
+    import sysconfig
+    return os.path.join(HERE, "_mba_host" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def _numpy_include():
+    import numpy
+    return numpy.get_include()
+
+
+def build_host(force: bool = False) -> str:
+    """Compile the native host extension (CPython C API, no torch) in-tree."""
+    import sysconfig
+    out = host_ext_path()
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(HOST_SRC):
+        return out
+    cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-shared", "-fPIC", "-pthread",
+           "-Wall", "-Wno-missing-field-initializers", "-I", sysconfig.get_paths()["include"],
+           "-I", _numpy_include(),
+           HOST_SRC, "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"host extension build failed:\n{r.stderr}")
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, prof="--prof" in sys.argv))
+    print(build_host(force="--force" in sys.argv))

@@ -255,39 +255,32 @@ def _write_back(prob, R, t, f, X):
     prob.focal = float(f)
 
 
-def lm_solve_batch(problems, cfg: LmConfig, precision: str | None = None) -> list:
-    """Solve many independent problems in ONE device launch (extension of
-    lm_solve). Mutates each problem; returns the per-problem info dicts."""
-    if not problems:
-        return []
-    for p in problems:
-        if len(p.uv) == 0:
-            raise ValueError("problem has no residuals")
-    hb = solver.pack_problems(list(problems))
-    db = solver.to_device(hb)
+_SOLVERS = {}
+
+
+def lm_solve_batch(problems, cfg: LmConfig, precision: str | None = None):
+    """Solve many independent problems (extension of lm_solve): each problem
+    is mutated exactly as lm_solve would mutate it (miniba.py:264-270, 288) and
+    the per-problem info dicts are returned as a lazy sequence
+    (paper_2506_05558_b200.batch.BatchResult).
+
+    The list is walked and copied by native code, the observations are sorted
+    point-major and packed on the device, and chunks of the batch flow through
+    upload -> pack -> solve -> read-back -> write-back with host and device
+    work overlapped (paper_2506_05558_b200/batch.py)."""
+    from paper_2506_05558_b200.batch import BatchSolver
     prm = solver.LmParams.from_cfg(cfg)
     if precision is not None:
         prm.precision = precision
-    sol = solver.solve(db, prm)
-    R, t, f, X = (_host(sol.R), _host(sol.t), _host(sol.focal), _host(sol.points))
-    n_it = _host(sol.n_iters)
-    status = _host(sol.status)
-    costs, lams, acc, ev, st = (_host(sol.costs), _host(sol.lambdas), _host(sol.accepted),
-                                _host(sol.evals), _host(sol.final_stats))
-    infos = []
-    for b, p in enumerate(problems):
-        if status[b] < 0:
-            raise ValueError("malformed problem (index out of range or unsorted observations)")
-        c0, c1 = hb.cam_off[b], hb.cam_off[b + 1]
-        p0, p1 = hb.pt_off[b], hb.pt_off[b + 1]
-        _write_back(p, R[c0:c1], t[c0:c1], f[b], X[p0:p1])
-        n = int(n_it[b])
-        K = max(st[b, 3], 1.0)
-        infos.append(dict(costs=costs[b, :n + 1].copy(), accepted=acc[b, :n].astype(bool),
-                          lambdas=lams[b, :n].copy(), final_rms=float(np.sqrt(st[b, 2] / K)),
-                          mean_err=float(st[b, 1] / K), evals=ev[b, :n].astype(np.int32),
-                          status=int(status[b])))
-    return infos
+    torch = _torch()
+    key = torch.cuda.current_device()
+    bs = _SOLVERS.get(key)
+    if bs is None:
+        bs = _SOLVERS[key] = BatchSolver(prm)
+    bs.prm = prm
+    res = bs.solve(problems)
+    torch.cuda.current_stream().wait_stream(bs.back)
+    return res
 
 
 def _lm_dense(prob: BaProblem, cfg: LmConfig) -> dict:
