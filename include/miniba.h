@@ -130,6 +130,25 @@ int32_t mba_pack_obs(int32_t n_problems, const int64_t* obs_off, const int64_t* 
                      MbaObs* out, float* out_lo, void* workspace, size_t workspace_bytes,
                      void* stream);
 
+/* The bootstrap schedule around lm_solve (miniba.py:782-805, run_schedule) as
+ * one device sequence over a batch of independent problems, no host round
+ * trip: mba_solve with cfg1 (first half of the iterations, out1) -> residual
+ * norms of that state and the robust filter e <= median + mad_factor * MAD
+ * (miniba.py:57-62), observations of points left with < 2 survivors dropped
+ * -> stable compaction into obs2 / obs_lo2 with offsets obs_off2 (n_kept per
+ * problem; 0 means the filter removed everything: BootstrapFailure) ->
+ * mba_solve with cfg2 continuing from out1's state (out2->*_in must equal
+ * out1->*_out) -> gauge: t and points scaled by 1 / mean pairwise camera
+ * distance (gauge_scale receives that distance; may be NULL). pt_alive[p] = 1
+ * for points that keep observations (the reference's surviving tracks). */
+size_t mba_bootstrap_workspace_bytes(const MbaBatchDesc* desc, const MbaLmConfig* cfg1);
+int32_t mba_bootstrap_schedule(const MbaBatchDesc* desc, const MbaLmConfig* cfg1,
+                               const MbaLmConfig* cfg2, double mad_factor, const MbaOutputs* out1,
+                               const MbaOutputs* out2, MbaObs* obs2, float* obs_lo2,
+                               int64_t* obs_off2, int64_t* n_kept, uint8_t* pt_alive,
+                               double* gauge_scale, void* workspace, size_t workspace_bytes,
+                               void* stream);
+
 int32_t mba_abi_version(void);
 
 /* Bytes of device workspace mba_solve needs for this batch and config. */

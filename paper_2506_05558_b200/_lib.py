@@ -89,6 +89,12 @@ def lib():
     L.mba_pack_obs_workspace_bytes.argtypes = [i64]
     L.mba_pack_obs.restype = i32
     L.mba_pack_obs.argtypes = [i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, sz, _vp]
+    L.mba_bootstrap_workspace_bytes.restype = sz
+    L.mba_bootstrap_workspace_bytes.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig)]
+    L.mba_bootstrap_schedule.restype = i32
+    L.mba_bootstrap_schedule.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig),
+                                         ct.POINTER(MbaLmConfig), d, ct.POINTER(MbaOutputs),
+                                         ct.POINTER(MbaOutputs), _vp, _vp, _vp, _vp, _vp, _vp, _vp, sz, _vp]
     if L.mba_abi_version() != 1:
         raise RuntimeError("libminiba ABI version mismatch")
     _lib = L
@@ -98,7 +104,7 @@ def lib():
 EXPORTED = ("mba_abi_version", "mba_workspace_bytes", "mba_solve", "mba_solve_plan", "mba_solve_launches", "mba_residuals", "mba_robust",
             "mba_blocks", "mba_assemble", "mba_solve_step_scratch_bytes", "mba_solve_step",
             "mba_pose_lm", "mba_triangulate", "mba_match_pairs", "mba_pack_obs_workspace_bytes",
-            "mba_pack_obs")
+            "mba_pack_obs", "mba_bootstrap_workspace_bytes", "mba_bootstrap_schedule")
 
 
 def check(rc, what):

@@ -15,7 +15,7 @@ SOURCES = [("mba_solve.cu", [], "mba_solve.o"), ("mba_v4.cu", [], "mba_v4_f64.o"
            ("mba_v4.cu", ["-DMBA_V4_F32"], "mba_v4_f32.o"), ("mba_stages.cu", [], "mba_stages.o"),
            ("mba_pose.cu", [], "mba_pose.o"), ("mba_tri.cu", [], "mba_tri.o"),
            ("mba_match.cu", [], "mba_match.o"),
-           ("mba_pack.cu", [], "mba_pack.o")]
+           ("mba_pack.cu", [], "mba_pack.o"), ("mba_bootstrap.cu", [], "mba_bootstrap.o")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -244,17 +244,6 @@ def solve_step(U, g_c, V, g_p, Wf, lam: float, method: str = "schur"):
 # ---------------------------------------------------------------------------
 # LM driver (miniba.py:223-296)
 
-def _write_back(prob, R, t, f, X):
-    for name, val in (("R", R), ("t", t), ("points", X)):
-        cur = getattr(prob, name)
-        if isinstance(cur, np.ndarray) and cur.dtype == np.float64 and cur.shape == val.shape \
-                and cur.flags.writeable:
-            cur[...] = val
-        else:
-            setattr(prob, name, val.copy())
-    prob.focal = float(f)
-
-
 _SOLVERS = {}
 
 
@@ -611,4 +600,5 @@ def align_bootstrap(new_poses: list, old_poses: list, new_points: np.ndarray, ob
     return aligned, pts, mean_err
 
 
-from ._bootstrap import bootstrap, build_tracks  # noqa: E402,F401
+from ._bootstrap import (bootstrap, bootstrap_batch, build_tracks, build_tracks_device,  # noqa: E402,F401
+                         default_matcher, filter_matches_flow)

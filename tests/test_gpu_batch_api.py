@@ -138,7 +138,7 @@ def test_lm_solve_batch_sorts_on_device(cuda_ok):
     b = make_batch(6, n_cams=8, K=2000, seed=17)
     a = _baproblems(b, range(6))
     sh = [_shuffled(b.problem(i), 100 + i) for i in range(6)]
-    s = [BaProblem(**q) for q in sh]
+    s = [BaProblem(**{k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in q.items()}) for q in sh]
     ia = lm_solve_batch(a, LmConfig(max_iters=200))
     is_ = lm_solve_batch(s, LmConfig(max_iters=200))
     host_sorted = run_device(sh, dict(max_iters=200), "f64")

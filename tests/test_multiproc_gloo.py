@@ -1,13 +1,14 @@
-"""CPU (gloo, world_size 2) test of the multi-GPU plumbing: contiguous shard
-ranges, per-shard problem generation, and the final all-gather of per-problem
-summaries in global order. The per-problem work here is the CPU oracle (tests
-may use it); on the GPU box the same code paths carry mba_solve results."""
+"""CPU (gloo, world_size 2) tests of the multi-GPU plumbing: contiguous shard
+ranges and the final gather of the COMPLETE per-problem outputs (R, t,
+focal, ragged points, final statistics, n_iters, status, LM traces) in global
+problem order (paper_2506_05558_b200/dist.py). On the GPU box the
+same code carries mba_solve outputs over NCCL (bench.py, and the one-GPU
+2-rank test in tests/test_gpu_dist.py)."""
 import os
 import socket
 import sys
 
 import numpy as np
-import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -15,6 +16,7 @@ import torch.multiprocessing as mp
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 N_PROBLEMS = 7
+MAX_ITERS = 5
 
 
 def _free_port():
@@ -23,19 +25,24 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _summaries(first, count):
-    from oracle import miniba_oracle as O
-    from paper_2506_05558_b200.synth import make_batch
-    b = make_batch(count, n_cams=4, K=240, seed=17, first=first)
-    stats, iters, status = [], [], []
-    for i in range(count):
-        info = O.lm(b.problem(i), max_iters=4)
-        e_sum = info["mean_err"] * 240
-        stats.append([info["cost"], e_sum, info["final_rms"], float(b.obs_off[i + 1] - b.obs_off[i])])
-        iters.append(len(info["accepted"]))
-        status.append(0)
-    return (torch.tensor(stats, dtype=torch.float64), torch.tensor(iters, dtype=torch.int32),
-            torch.tensor(status, dtype=torch.int32))
+def _fake_outputs(first, count):
+    """Deterministic stand-in for a shard's Solution: problem i has 3 + i % 3
+    cameras and 10 + 7 * i points, values derived from the global index."""
+    n = [3 + (first + i) % 3 for i in range(count)]
+    P = [10 + 7 * (first + i) for i in range(count)]
+    g = lambda i, k: np.float64(1000 * (first + i) + k)
+    R = np.concatenate([np.full((n[i], 9), g(i, 1)) for i in range(count)])
+    t = np.concatenate([np.full((n[i], 3), g(i, 2)) for i in range(count)])
+    X = np.concatenate([np.arange(3 * P[i], dtype=np.float64) + g(i, 3) for i in range(count)])
+    out = dict(R=R, t=t, points=X, focal=np.array([g(i, 4) for i in range(count)]),
+               final_stats=np.array([[g(i, 5 + j) for j in range(4)] for i in range(count)]),
+               n_iters=np.array([first + i for i in range(count)], np.int32),
+               status=np.array([(first + i) % 3 for i in range(count)], np.int32),
+               costs=np.array([[g(i, 10 + j) for j in range(MAX_ITERS + 1)] for i in range(count)]),
+               lambdas=np.array([[g(i, 20 + j) for j in range(MAX_ITERS)] for i in range(count)]),
+               accepted=np.array([[(first + i + j) % 2 for j in range(MAX_ITERS)] for i in range(count)], np.uint8),
+               evals=np.array([[(first + i + j) % 6 for j in range(MAX_ITERS)] for i in range(count)], np.uint8))
+    return {k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in out.items()}, sum(n), sum(P)
 
 
 def _worker(rank, world, port, out_path):
@@ -44,12 +51,12 @@ def _worker(rank, world, port, out_path):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2506_05558_b200 import dist as mdist
     lo, hi = mdist.shard_range(N_PROBLEMS, rank, world)
-    fs, it, st = _summaries(lo, hi - lo)
-    rows = mdist.padded_rows(N_PROBLEMS, world)
-    local = mdist.pack_summary(torch, fs, it, st, rows, "cpu")
-    full = mdist.gather_summaries(torch, dist, local, N_PROBLEMS, world)
+    outs, C, P = _fake_outputs(lo, hi - lo)
+    g = mdist.OutputGather(torch, dist, (hi - lo, C, P), MAX_ITERS, torch.device("cpu"))
+    for _ in range(2):   # the buffers are reused step after step
+        full = g.gather(outs)
     if rank == 0:
-        np.save(out_path, full.numpy())
+        np.savez(out_path, **{k: v.numpy() for k, v in full.items()})
     dist.barrier()
     dist.destroy_process_group()
 
@@ -64,12 +71,17 @@ def test_shard_ranges_cover_the_batch():
             assert max(h - l for l, h in got) - min(h - l for l, h in got) <= 1
 
 
-def test_two_rank_gloo_gather_matches_single_process(tmp_path):
-    out = str(tmp_path / "gathered.npy")
+def test_two_rank_gloo_gather_of_full_outputs(tmp_path):
+    out = str(tmp_path / "gathered.npz")
     mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
-    gathered = np.load(out)
+    got = np.load(out)
+    single, _, _ = _fake_outputs(0, N_PROBLEMS)
+    for k, v in single.items():
+        np.testing.assert_array_equal(got[k], v.numpy().reshape(-1), err_msg=k)
+
+
+def test_field_counts():
     from paper_2506_05558_b200 import dist as mdist
-    fs, it, st = _summaries(0, N_PROBLEMS)
-    single = mdist.pack_summary(torch, fs, it, st, N_PROBLEMS, "cpu").numpy()
-    assert gathered.shape == (N_PROBLEMS, mdist.SUMMARY_WIDTH)
-    np.testing.assert_array_equal(gathered, single)   # shard-invariant, bit for bit
+    c = mdist.field_counts(4, 32, 1000, 200)
+    assert c["R"] == 288 and c["points"] == 3000 and c["costs"] == 4 * 201 and c["evals"] == 800
+    assert "costs" not in mdist.field_counts(4, 32, 1000, 200, traces=False)
