@@ -57,7 +57,7 @@ constexpr int kUcamStride = 45;  // per free camera: U_aa lower(21) U_af(6) g_a(
 // Optional per-phase cycle counters (build with -DMBA_PHASE_PROF; see
 // paper_2506_05558_b200/build.py --prof). Thread 0 of every CTA accumulates
 // clock64() deltas between phase boundaries; totals land in g_prof[phase].
-enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_N };
+enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_JWAIT, PH_JRED, PH_ITEMS, PH_ITEMS2, PH_NCAM, PH_NPAIR, PH_N };
 #ifdef MBA_PHASE_PROF
 __device__ unsigned long long* g_prof = nullptr;
 #define PROF_DECL __shared__ long long s_prof[PH_N]; long long prof_t = clock64(); \
@@ -79,6 +79,7 @@ struct SolveParams {
   size_t ws_slot_bytes;
   int max_cams;
   unsigned char* grid;     // cooperative (multi-CTA) mode: cross-CTA buffers
+  int64_t grid_chunks;     // capacity of the job-chunk tables in `grid`
   int only_flagged;        // solve only problems the cluster kernel could not place
 };
 
@@ -106,8 +107,9 @@ struct Layout {
   static constexpr size_t oDc = oTt + 8 * 3 * N * kBacktrackTries;  // double[C]
   static constexpr size_t oRed = align16(oDc + 8 * C);              // double[kWarps*4]
   static constexpr size_t oS = oRed + 8 * kWarps * 4;               // T[CA]
-  static constexpr size_t oRhs = align16(oS + sizeof(T) * CA);      // T[C] (solution scratch)
-  static constexpr size_t oTab = align16(oRhs + sizeof(T) * C);     // uint16[CA] (row << 8 | col)
+  static constexpr size_t oRhs = align16(oS + sizeof(T) * CA);      // T[C] LDL^T pivot reciprocals
+  static constexpr size_t oL10 = align16(oRhs + sizeof(T) * C);     // T[C] LDL^T pair multipliers
+  static constexpr size_t oTab = align16(oL10 + sizeof(T) * C);     // uint16[CA] (row << 8 | col)
   static constexpr size_t oUcam = align16(oTab + 2 * CA);           // T[N][kUcamStride]
   static constexpr size_t oCamPtr = align16(oUcam + sizeof(T) * N * kUcamStride);
   static constexpr size_t oSlot = oCamPtr + 4 * (N + 1);
@@ -302,14 +304,34 @@ __device__ __forceinline__ Scratch<T, RES> scratch_at(unsigned char* base, const
 }
 
 // Cross-CTA buffers of the cooperative mode (one problem spread over the grid).
+// Cooperative mode: work chunks of the camera / pair jobs (spread over every
+// warp of the grid; a camera job is split into runs of kChunkObs observations,
+// a pair block into runs of kChunkPairs co-observation pairs) and their partial
+// sums, reduced per job in chunk order (deterministic).
+constexpr int kChunkObs = 256;
+constexpr int kChunkPairs = 512;
+
+__host__ __device__ inline int64_t grid_max_chunks(int64_t max_obs, int64_t max_pairs, int maxc) {
+  return (max_obs + kChunkObs - 1) / kChunkObs + maxc + (max_pairs + kChunkPairs - 1) / kChunkPairs +
+         (int64_t)maxc * (maxc + 1) / 2;
+}
+
+// Cross-CTA buffers of the cooperative mode (one problem spread over the grid).
 template <typename T, int MAXC>
 struct GridBufs {
   static constexpr int C = 6 * MAXC + 1, CA = C * (C + 3) / 2, NB = MAXC * (MAXC + 1) / 2;
   static constexpr size_t oS = 0;                                     // T[CA]
   static constexpr size_t oU = align16(oS + sizeof(T) * CA);          // T[MAXC][kUcamStride]
   static constexpr size_t oCnt = align16(oU + sizeof(T) * MAXC * kUcamStride);  // int[MAXC + NB + 2]
-  static constexpr size_t oRed = align16(oCnt + 4 * (MAXC + NB + 2)); // double[2][G][4]
-  static __host__ __device__ size_t bytes(int G) { return oRed + 8 * 2 * 4 * (size_t)G; }
+  static constexpr size_t oCoff = align16(oCnt + 4 * (MAXC + NB + 2));  // int[MAXC + NB + 1] chunks per job
+  static constexpr size_t oRed = align16(oCoff + 4 * (MAXC + NB + 1));  // double[2][G][4]
+  static __host__ __device__ size_t oChunk(int G) { return align16(oRed + 8 * 2 * 4 * (size_t)G); }  // int2[chunks]
+  static __host__ __device__ size_t oPart(int G, int64_t chunks) {   // T[chunks][kUcamStride]
+    return align16(oChunk(G) + 8 * (size_t)chunks);
+  }
+  static __host__ __device__ size_t bytes(int G, int64_t chunks) {
+    return oPart(G, chunks) + sizeof(T) * kUcamStride * (size_t)chunks;
+  }
 };
 
 template <typename T, int MAXC, bool RES, bool GRID = false, int NT = kThreads>
@@ -524,6 +546,24 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     for (int i = j; i <= C; ++i) sm.tab[a0 + i - j] = (unsigned short)((i << 8) | j);
   }
   const int CA = C * (C + 3) / 2;
+  // cooperative mode: the job chunk table (job, first item) and chunks per job
+  int* coff = GRID ? (int*)(P.grid + GB::oCoff) : nullptr;
+  int2* chunk = GRID ? (int2*)(P.grid + GB::oChunk(nranks)) : nullptr;
+  T* cpart = GRID ? (T*)(P.grid + GB::oPart(nranks, P.grid_chunks)) : nullptr;
+  if constexpr (GRID) {
+    if (rank == 0 && tid == 0) {
+      int q = 0;
+      coff[0] = 0;
+      for (int job = 0; job < nf + nb; ++job) {
+        const int len = job < nf ? sm.cam_ptr[sm.cam_of_slot[job] + 1] - sm.cam_ptr[sm.cam_of_slot[job]]
+                                 : sm.blk_off[job - nf + 1] - sm.blk_off[job - nf];
+        const int ch = job < nf ? kChunkObs : kChunkPairs;
+        for (int lo_i = 0; lo_i < len && q < P.grid_chunks; lo_i += ch) chunk[q++] = make_int2(job, lo_i);
+        coff[job + 1] = q;
+      }
+    }
+    gsync();
+  }
   double f = O.focal_in[b];
   if (s_flag) {  // malformed problem: report and leave parameters untouched
     if (lead) {
@@ -651,17 +691,43 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     // (block_sum ended with __syncthreads: point factors are visible)
     PROF_MARK(PH_POINT)
 
-    // ---------- K2 camera jobs + K3 pair jobs (one warp per job) ----------
+    // ---------- K2 camera jobs + K3 pair jobs ----------
+    // batched mode: one warp per job; cooperative mode: one warp per job CHUNK
+    // (every warp of the grid busy), partial sums reduced per job afterwards
     T* S_jobs = GRID ? (T*)(P.grid + GB::oS) : sm.S;
     T* U_jobs = GRID ? (T*)(P.grid + GB::oU) : sm.ucam;
-    for (int job = gwid; job < nf + nb; job += gwarps) {
+    const int n_items = GRID ? coff[nf + nb] : nf + nb;
+    for (int item = gwid; item < n_items; item += gwarps) {
+      // reconverge the warp before the lane-strided loops: without it the lanes
+      // that left the previous item's loop at different trip counts stay
+      // split and the loop runs with ~2 of 32 lanes active (measured)
+      __syncwarp();
+      int job = item, q_lo = 0, q_hi = 0;
+      if constexpr (GRID) {
+        const int2 cj = chunk[item];
+        job = cj.x;
+        q_lo = cj.y;
+      }
+#ifdef MBA_PHASE_PROF
+      long long t_item;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item));
+#endif
       if (job < nf) {
         const int s = job, c = sm.cam_of_slot[s];
         const double* Rk = sm.Rc + 9 * c;
         T acc[kUcamStride];
 #pragma unroll
         for (int i = 0; i < kUcamStride; ++i) acc[i] = T(0);
-        for (int q = sm.cam_ptr[c] + lane; q < sm.cam_ptr[c + 1]; q += 32) {
+        int qa = sm.cam_ptr[c], qb = sm.cam_ptr[c + 1];
+        if constexpr (GRID) {
+          qa += q_lo;
+          q_hi = qa + kChunkObs;
+          qb = q_hi < qb ? q_hi : qb;
+        }
+        for (int q0 = qa; q0 < qb; q0 += 32) {
+          __syncwarp();
+          const int q = q0 + lane;
+          if (q >= qb) continue;
           const int k = perm[q];
           Obs o = load_obs(obs, lo, k);
           const double Xp[3] = {X[3 * o.pt], X[3 * o.pt + 1], X[3 * o.pt + 2]};
@@ -694,16 +760,35 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
         }
 #pragma unroll
         for (int i = 0; i < kUcamStride; ++i) acc[i] = warp_sum(acc[i]);
-        if (lane == 0)
-          for (int i = 0; i < kUcamStride; ++i) U_jobs[s * kUcamStride + i] = acc[i];
+        T* dst = GRID ? cpart + (size_t)item * kUcamStride : U_jobs + s * kUcamStride;
+#pragma unroll
+        for (int i = 0; i < kUcamStride; ++i)
+          if ((i & 31) == lane) dst[i] = acc[i];
       } else {
         const int blk = job - nf;
         const int sa = sm.blk_a[blk], sb = sm.blk_b[blk];
         T acc[36];
 #pragma unroll
         for (int i = 0; i < 36; ++i) acc[i] = T(0);
-        const int q1 = sm.blk_off[blk + 1];
-        for (int q = sm.blk_off[blk] + lane; q < q1; q += 32) {
+        int qa = sm.blk_off[blk], q1 = sm.blk_off[blk + 1];
+        if constexpr (GRID) {
+          qa += q_lo;
+          q_hi = qa + kChunkPairs;
+          q1 = q_hi < q1 ? q_hi : q1;
+        }
+        for (int q0 = qa; q0 < q1; q0 += 32) {
+          __syncwarp();
+          const int q = q0 + lane;
+          if (q >= q1) continue;
+#ifdef MBA_PHASE_PROF
+          {
+            const unsigned am = __activemask();
+            if (tid == 0) {
+              s_prof[PH_NCAM] += __popc(am);
+              s_prof[PH_NPAIR] += 1;
+            }
+          }
+#endif
           const int2 pr = W.pair(q);
           T yi[18], yj[18];
           ld18(Ybuf + (size_t)pr.x * YSTR, yi);
@@ -717,28 +802,65 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
         }
 #pragma unroll
         for (int i = 0; i < 36; ++i) acc[i] = warp_sum(acc[i]);
-        // acc[r][cc] = S(6sa + r, 6sb + cc); stored in the lower triangle, lanes
-        // writing disjoint entries
+        if constexpr (GRID) {
+          T* dst = cpart + (size_t)item * kUcamStride;
 #pragma unroll
-        for (int i = 0; i < 36; ++i) {
-          if ((i & 31) != lane) continue;
-          const int r = i / 6, cc = i % 6;
-          if (sa == sb) {
-            if (cc <= r) S_jobs[acol(6 * sa + cc, C) + r - cc] = -acc[i];
-          } else {
-            const int row = 6 * sb + cc, col = 6 * sa + r;
-            S_jobs[acol(col, C) + row - col] = -acc[i];
+          for (int i = 0; i < 36; ++i)
+            if ((i & 31) == lane) dst[i] = acc[i];
+        } else {
+          // acc[r][cc] = S(6sa + r, 6sb + cc); stored in the lower triangle, lanes
+          // writing disjoint entries
+#pragma unroll
+          for (int i = 0; i < 36; ++i) {
+            if ((i & 31) != lane) continue;
+            const int r = i / 6, cc = i % 6;
+            if (sa == sb) {
+              if (cc <= r) S_jobs[acol(6 * sa + cc, C) + r - cc] = -acc[i];
+            } else {
+              const int row = 6 * sb + cc, col = 6 * sa + r;
+              S_jobs[acol(col, C) + row - col] = -acc[i];
+            }
           }
         }
       }
+#ifdef MBA_PHASE_PROF
+      if (tid == 0) {
+        long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        s_prof[job < nf ? PH_ITEMS : PH_ITEMS2] += t_end - t_item;
+        (void)0;
+      }
+#endif
     }
+    PROF_MARK(PH_JOBS)
     gsync();
+    PROF_MARK(PH_JWAIT)
     if constexpr (GRID) {
+      // per-job totals of the chunk partials, in chunk order
+      const int nu = nf * kUcamStride;
+      for (int it2 = gtid; it2 < nu + nb * 36; it2 += gthreads) {
+        const int job = it2 < nu ? it2 / kUcamStride : nf + (it2 - nu) / 36;
+        const int i = it2 < nu ? it2 % kUcamStride : (it2 - nu) % 36;
+        T v = T(0);
+        for (int q = coff[job]; q < coff[job + 1]; ++q) v += cpart[(size_t)q * kUcamStride + i];
+        if (job < nf) {
+          U_jobs[job * kUcamStride + i] = v;
+        } else {
+          const int blk = job - nf, sa = sm.blk_a[blk], sb = sm.blk_b[blk], r = i / 6, cc = i % 6;
+          if (sa == sb) {
+            if (cc <= r) S_jobs[acol(6 * sa + cc, C) + r - cc] = -v;
+          } else {
+            const int row = 6 * sb + cc, col = 6 * sa + r;
+            S_jobs[acol(col, C) + row - col] = -v;
+          }
+        }
+      }
+      gsync();
       for (int i = tid; i < CA; i += blockDim.x) sm.S[i] = S_jobs[i];
       for (int i = tid; i < nf * kUcamStride; i += blockDim.x) sm.ucam[i] = U_jobs[i];
       __syncthreads();
     }
-    PROF_MARK(PH_JOBS)
+    PROF_MARK(PH_JRED)
 
     // ---------- assemble damped S and rhs (miniba.py:188-213) ----------
     if (!opt_pts) {
@@ -768,42 +890,140 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     __syncthreads();
     PROF_MARK(PH_ASM)
 
-    // ---------- K4 LDL^T of the augmented system, one barrier per column ----------
-    // Elimination of column k updates every later column and its rhs row with
-    // all threads over the flat packed range (tab gives row/column); the rhs row
-    // ends up holding the forward-substituted y. S[k][k] keeps d_k, S[i][k] keeps
-    // L_ik d_k.
+    // ---------- K4 LDL^T of the augmented system, two pivots per barrier ----------
+    // Right-looking rank-2 steps (as in mba_v4.cu): pivots k and k+1 are formed
+    // redundantly by every thread, the trailing entries (columns >= k+2, a
+    // contiguous packed range; tab gives row / column) receive both updates at
+    // once with column k+1 corrected on the fly, and column k+1 is finalised
+    // lazily during the next step. The rhs row ends up holding the forward-
+    // substituted y; S[k][k] keeps d_k, S[i][k] keeps L_ik d_k, invd[k] = 1/d_k.
     bool chol_fail = false;
-    for (int k = 0; k < C; ++k) {
-      const T* colk = sm.S + acol(k, C) - k;  // colk[i] = S[i][k], i in [k, C]
-      const T d = colk[k];
-      if (!(d > T(0)) || !isfinite((double)d)) {
-        chol_fail = true;  // every thread reads the same pivot: uniform exit
-        break;
+    {
+      T* invd = sm.rhs;
+      T* l10s = (T*)(smem_raw + L::oL10);
+      auto bad_pivot = [](T d) { return !(d > T(0)) || !isfinite((double)d); };
+      int k = 0, pend = -1;
+      for (; k + 1 < C; k += 2) {
+        const T* colk = sm.S + acol(k, C) - k;
+        const T* colk1 = sm.S + acol(k + 1, C) - (k + 1);
+        const T d0 = colk[k], a10 = colk[k + 1], d1r = colk1[k + 1];
+        if (bad_pivot(d0)) {
+          chol_fail = true;
+          break;
+        }
+        const T i0 = T(1) / d0;
+        const T l10 = a10 * i0;
+        const T d1 = d1r - l10 * a10;
+        if (bad_pivot(d1)) {
+          chol_fail = true;
+          break;
+        }
+        const T i1 = T(1) / d1;
+        if (tid == 0) {
+          invd[k] = i0;
+          invd[k + 1] = i1;
+          l10s[k] = l10;
+        }
+        // four entries per thread in flight (the loads form short dependent
+        // chains: tab -> column entries -> update)
+        const int e0 = acol(k + 2, C) + tid;
+        const int NTB = blockDim.x;
+        int e = e0;
+        for (; e + 3 * NTB < CA; e += 4 * NTB) {
+          unsigned ij[4];
+          T ai[4], aj[4], ci[4], cj[4], sv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) ij[u] = sm.tab[e + u * NTB];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ii = (int)(ij[u] >> 8), jj = (int)(ij[u] & 255u);
+            ai[u] = colk[ii];
+            aj[u] = colk[jj];
+            ci[u] = colk1[ii];
+            cj[u] = colk1[jj];
+            sv[u] = sm.S[e + u * NTB];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const T ci1 = ci[u] - ai[u] * l10, cj1 = cj[u] - aj[u] * l10;
+            sm.S[e + u * NTB] = sv[u] - ai[u] * aj[u] * i0 - ci1 * cj1 * i1;
+          }
+        }
+        for (; e < CA; e += NTB) {
+          const unsigned ij = sm.tab[e];
+          const int ii = (int)(ij >> 8), jj = (int)(ij & 255u);
+          const T ai = colk[ii], aj = colk[jj], ci = colk1[ii], cj = colk1[jj];
+          const T ci1 = ci - ai * l10, cj1 = cj - aj * l10;
+          sm.S[e] = sm.S[e] - ai * aj * i0 - ci1 * cj1 * i1;
+        }
+        if (pend >= 0) {   // finalise column pend (= k - 1) against column pend - 1
+          T* cp = sm.S + acol(pend, C) - pend;
+          const T* cq = sm.S + acol(pend - 1, C) - (pend - 1);
+          const T lp = l10s[pend - 1];
+          for (int i = pend + tid; i <= C; i += blockDim.x) cp[i] = cp[i] - cq[i] * lp;
+        }
+        pend = k + 1;
+        __syncthreads();
       }
-      const T inv = T(1) / d;
-      for (int e = acol(k + 1, C) + tid; e < CA; e += blockDim.x) {
-        const unsigned ij = sm.tab[e];
-        sm.S[e] -= colk[ij >> 8] * colk[ij & 255u] * inv;
+      if (!chol_fail) {
+        if (pend >= 0) {
+          T* cp = sm.S + acol(pend, C) - pend;
+          const T* cq = sm.S + acol(pend - 1, C) - (pend - 1);
+          const T lp = l10s[pend - 1];
+          for (int i = pend + tid; i <= C; i += blockDim.x) cp[i] = cp[i] - cq[i] * lp;
+          __syncthreads();
+        }
+        if (k < C) {   // odd C: the last pivot alone
+          const T* colk = sm.S + acol(k, C) - k;
+          const T d = colk[k];
+          if (bad_pivot(d)) {
+            chol_fail = true;
+          } else {
+            const T inv = T(1) / d;
+            for (int e = acol(k + 1, C) + tid; e < CA; e += blockDim.x) {
+              const unsigned ij = sm.tab[e];
+              sm.S[e] -= colk[ij >> 8] * colk[ij & 255u] * inv;
+            }
+            if (tid == 0) invd[k] = inv;
+          }
+          __syncthreads();
+        }
       }
-      __syncthreads();
     }
     if (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull)) chol_fail = true;
     PROF_MARK(PH_CHOL)
 
     if (!chol_fail) {
-      // back substitution x_k = (y_k - sum_{i>k} S[i][k] x_i) / d_k in warp 0
+      // column-oriented back substitution D L^T x = y in warp 0 (no
+      // reductions): x_k = u_k / d_k, then u_j -= S[k][j] x_k for j < k
       if (wid == 0) {
-        for (int k = C - 1; k >= 0; --k) {
-          const T* colk = sm.S + acol(k, C) - k;
-          T acc = T(0);
-          for (int i = k + 1 + lane; i < C; i += 32) acc += colk[i] * sm.rhs[i];
-          acc = warp_sum(acc);
-          const T xk = (colk[C] - acc) / colk[k];
-          if (lane == 0) sm.rhs[k] = xk;
-          __syncwarp();
+        constexpr int NU = (6 * MAXC + 1 + 31) / 32;
+        const T* invd = sm.rhs;
+        T u[NU];
+#pragma unroll
+        for (int q = 0; q < NU; ++q) {
+          const int j = lane + 32 * q;
+          u[q] = j < C ? sm.S[acol(j, C) + C - j] : T(0);
         }
-        for (int i = lane; i < C; i += 32) sm.dc[i] = (double)sm.rhs[i];
+        for (int k = C - 1; k >= 0; --k) {
+          const int qk = k >> 5;
+          T uk = T(0);
+#pragma unroll
+          for (int q = 0; q < NU; ++q)
+            if (q == qk) uk = __shfl_sync(0xffffffffu, u[q], k & 31);
+          const T xk = uk * invd[k];
+#pragma unroll
+          for (int q = 0; q < NU; ++q) {
+            const int j = lane + 32 * q;
+            if (q == qk && lane == (k & 31)) u[q] = xk;
+            if (j < k) u[q] -= sm.S[acol(j, C) + k - j] * xk;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NU; ++q) {
+          const int j = lane + 32 * q;
+          if (j < C) sm.dc[j] = (double)u[q];
+        }
       }
       __syncthreads();
       // back substitution for the points (miniba.py:217)
@@ -980,7 +1200,12 @@ static int launch_grid(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaO
   // enough observations per CTA to amortise the grid barriers
   const int64_t want = (d->max_obs + 511) / 512;
   if (want < grid) grid = (int)(want < 1 ? 1 : want);
-  const size_t gbytes = align16(GridBufs<T, MAXC>::bytes(grid));
+  if (const char* e = getenv("MBA_GRID_CTAS")) {   // experiments: fewer CTAs
+    const int v = atoi(e);
+    if (v > 0 && v < grid) grid = v;
+  }
+  const int64_t chunks = grid_max_chunks(d->max_obs, d->max_pairs, MAXC);
+  const size_t gbytes = align16(GridBufs<T, MAXC>::bytes(grid, chunks));
   if (ws_bytes < 256 + scratch + gbytes) return MBA_ERR_INVALID;
   SolveParams P;
   P.d = *d;
@@ -991,6 +1216,7 @@ static int launch_grid(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaO
   P.ws_slot_bytes = scratch;
   P.max_cams = d->max_cams;
   P.grid = P.ws + align16(scratch);
+  P.grid_chunks = chunks;
   void* args[] = {&P};
   cudaLaunchCooperativeKernel((void*)solve_grid_kernel<T, MAXC>, dim3(grid), dim3(kThreads), args, smem, st);
   return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
@@ -1132,7 +1358,8 @@ size_t mba_workspace_bytes(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
   const bool f64 = cfg->precision == MBA_LIN_F64;
   const size_t slot = f64 ? mba::scratch_bytes<double, false>(d->max_obs, d->max_points, d->max_pairs)
                           : mba::scratch_bytes<float, false>(d->max_obs, d->max_points, d->max_pairs);
-  const size_t gextra = mba::align16(mba::GridBufs<double, 32>::bytes(n_sm)) + 256;
+  const size_t gextra =
+      mba::align16(mba::GridBufs<double, 32>::bytes(n_sm, mba::grid_max_chunks(d->max_obs, d->max_pairs, 32))) + 256;
   // one scratch slot per resident CTA of the CTA kernel (bounded by the batch)
   // plus the cooperative grid mode's cross-CTA buffers
   size_t grid = (size_t)n_sm * 16;

@@ -110,7 +110,12 @@ __host__ __device__ constexpr size_t pt_bytes() { return 24 + sizeof(T) * PSTR +
 
 // Optional per-phase cycle counters (-DMBA_PHASE_PROF, scripts/phase_prof.py):
 // thread 0 of every CTA accumulates clock64() deltas between phase marks.
-enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_CHA, PH_CHB, PH_N };
+enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_CHA, PH_CHB, PH_LCAM, PH_NCAM, PH_LPAIR, PH_NPAIR, PH_N };
+#ifdef MBA_PHASE_PROF
+#define LANES_PROF(sum_slot, n_slot) { const unsigned am_ = __activemask(); if (threadIdx.x == 0) { s_prof[sum_slot] += __popc(am_); s_prof[n_slot] += 1; } }
+#else
+#define LANES_PROF(sum_slot, n_slot)
+#endif
 #ifdef MBA_PHASE_PROF
 static __device__ unsigned long long* g_prof = nullptr;
 #define PROF_DECL __shared__ long long s_prof[PH_N]; long long prof_t = clock64(); \
@@ -957,7 +962,15 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         T acc[UST];
 #pragma unroll
         for (int i = 0; i < UST; ++i) acc[i] = T(0);
-        for (int q = cam_ptr[c] + lane; q < cam_ptr[c + 1]; q += 32) {
+        // uniform trip count + __syncwarp per step: the lane-strided loop
+        // otherwise ran with ~9 of 32 lanes active (lanes never reconverged
+        // after the previous job; measured with LANES_PROF)
+        const int qa = cam_ptr[c], qb = cam_ptr[c + 1];
+        for (int q0 = qa; q0 < qb; q0 += 32) {
+          __syncwarp();
+          const int q = q0 + lane;
+          if (q >= qb) continue;
+          LANES_PROF(PH_LCAM, PH_NCAM)
           const int kl = perm[q];
           const float4 ob = sobs[kl];
           const int sl = __float_as_int(ob.w);
@@ -1034,7 +1047,11 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
 #pragma unroll
         for (int i = 0; i < 36; ++i) acc[i] = T(0);
         const int q1 = blk_off[blk + 1];
-        for (int q = blk_off[blk] + lane; q < q1; q += 32) {
+        for (int q0 = blk_off[blk]; q0 < q1; q0 += 32) {
+          __syncwarp();
+          const int q = q0 + lane;
+          if (q >= q1) continue;
+          LANES_PROF(PH_LPAIR, PH_NPAIR)
           const unsigned pr = pairs[q];
           const int i = (int)(pr >> 16), j = (int)(pr & 0xffffu);
           const int sl = __float_as_int(sobs[i].w);

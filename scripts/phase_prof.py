@@ -13,9 +13,12 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [REPO, os.path.join(REPO, "src")]
 os.environ["MBA_LIB"] = os.environ.get("MBA_PROF_LIB") or os.path.join(REPO, "paper_2506_05558_b200", "libminiba_prof.so")
 
+# index -> phase; the cluster kernel (mba_v4.cu) and the CTA / grid kernels
+# (mba_solve.cu) share 0-8; 9-10 are ldl-core / unused (v4) and
+# jobs-barrier-wait / job-reduction (grid mode)
 PHASES = ["setup", "cost0", "point", "jobs", "assemble", "cholesky", "solve+backsub", "trials", "commit",
-          "ldl", "unused", "setup_stage_validate", "setup_slots_X", "setup_perm", "setup_pairs",
-          "setup_jobs_tab"]
+          "ldl|jobs_wait", "jobs_reduce", "setup_stage_validate|cam_chunks_cyc", "setup_slots_X|pair_chunks_cyc",
+          "setup_perm|n_cam_chunks", "setup_pairs|n_pair_chunks", "setup_jobs_tab"]
 
 
 def main():
