@@ -244,11 +244,16 @@ int32_t mba_triangulate(int32_t n_tracks, const int64_t* obs_off, const int32_t*
  * frame_a / frame_b; max_rows >= the largest frame. Per row of frame_a:
  * match_b (index in frame_b of the mutual ratio-tested nearest neighbour, or -1)
  * and dist (its Hamming distance); nn_ab/ok_a/best_ab/nn_ba/ok_b are the
- * per-direction scratch results (caller-sized like the row offsets). */
+ * per-direction scratch results (caller-sized like the row offsets: rows_a /
+ * rows_b entries). Every distance is computed once (64 x 64 tiles with row and
+ * column partial minima); workspace >= mba_match_workspace_bytes(rows_a,
+ * rows_b, max_rows) bytes holds the partials. */
+size_t mba_match_workspace_bytes(int64_t rows_a, int64_t rows_b, int64_t max_rows);
 int32_t mba_match_pairs(int32_t n_frames, const uint8_t* desc, const int64_t* desc_off, int32_t n_pairs,
                         const int32_t* pairs, const int64_t* row_off_a, const int64_t* row_off_b,
                         int64_t max_rows, double ratio_max, int32_t* nn_ab, uint8_t* ok_a, int32_t* best_ab,
-                        int32_t* nn_ba, uint8_t* ok_b, int32_t* match_b, int32_t* dist, void* stream);
+                        int32_t* nn_ba, uint8_t* ok_b, int32_t* match_b, int32_t* dist, int64_t rows_a,
+                        int64_t rows_b, void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

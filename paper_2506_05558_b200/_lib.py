@@ -62,7 +62,9 @@ def lib():
     L.mba_solve_plan.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig)]
     L.mba_match_pairs.restype = i32
     L.mba_match_pairs.argtypes = [i32, _vp, _vp, i32, _vp, _vp, _vp, i64, d, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                                  _vp]
+                                  i64, i64, _vp, sz, _vp]
+    L.mba_match_workspace_bytes.restype = sz
+    L.mba_match_workspace_bytes.argtypes = [i64, i64, i64]
     L.mba_triangulate.restype = i32
     L.mba_triangulate.argtypes = [i32, _vp, _vp, _vp, i32, _vp, _vp, d, d, d, d, d, i32, _vp, _vp, _vp, _vp]
     L.mba_solve_launches.restype = i32
@@ -103,7 +105,7 @@ def lib():
 
 EXPORTED = ("mba_abi_version", "mba_workspace_bytes", "mba_solve", "mba_solve_plan", "mba_solve_launches", "mba_residuals", "mba_robust",
             "mba_blocks", "mba_assemble", "mba_solve_step_scratch_bytes", "mba_solve_step",
-            "mba_pose_lm", "mba_triangulate", "mba_match_pairs", "mba_pack_obs_workspace_bytes",
+            "mba_pose_lm", "mba_triangulate", "mba_match_pairs", "mba_match_workspace_bytes", "mba_pack_obs_workspace_bytes",
             "mba_pack_obs", "mba_bootstrap_workspace_bytes", "mba_bootstrap_schedule")
 
 

@@ -108,6 +108,18 @@ class BatchResult:
         for b in range(len(self)):
             yield self[b]
 
+    def set(self, b, info):
+        """Store problem b's info dict (problems solved outside the batch)."""
+        n = len(info["accepted"])
+        self.costs[b, :n + 1] = info["costs"]
+        self.accepted[b, :n] = info["accepted"]
+        self.lambdas[b, :n] = info["lambdas"]
+        self.evals[b, :n] = info.get("evals", np.zeros(n))
+        self.n_iters[b] = n
+        self.status[b] = info.get("status", -3)
+        K = 1.0
+        self.final_stats[b] = (info["costs"][-1], info["mean_err"] * K, info["final_rms"] ** 2 * K, K)
+
 
 _OUT = ("R", "t", "focal", "points", "costs", "lambdas", "accepted", "evals", "n_iters", "status",
         "final_stats")

@@ -1249,34 +1249,11 @@ static int launch_cfg(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOu
   P.max_cams = d->max_cams;
   P.only_flagged = only_flagged;
   cudaMemsetAsync(ws, 0, sizeof(int), st);
-  // Keep the per-CTA scratch slots resident in L2 (persisting window) while
-  // the observation stream passes through; the caller's stream attribute is
-  // restored after the launch.
-  cudaStreamAttrValue old_attr{}, attr{};
-  bool windowed = false;
-  if (!RES) {
-    int max_win = 0, max_persist = 0;
-    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    const size_t want = scratch * (size_t)grid;
-    if (max_win > 0 && max_persist > 0 &&
-        cudaStreamGetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &old_attr) == cudaSuccess) {
-      size_t limit = 0;
-      cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize);
-      if (limit < (size_t)max_persist) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
-      attr.accessPolicyWindow.base_ptr = P.ws;
-      attr.accessPolicyWindow.num_bytes = want < (size_t)max_win ? want : (size_t)max_win;
-      attr.accessPolicyWindow.hitRatio = 1.0f;
-      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      windowed = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr) == cudaSuccess;
-    }
-    cudaGetLastError();
-  }
+  // (no persisting-L2 window: a process-wide carve-out would outlive this
+  // call and shrink L2 for the caller's own kernels; the scratch slots are
+  // L2-resident at the sizes this path serves anyway)
   solve_kernel<T, MAXC, RES, NT, MINB><<<grid, NT, smem, st>>>(P);
-  const cudaError_t err = cudaGetLastError();
-  if (windowed) cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &old_attr);
-  return err == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
+  return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
 }
 
 // Shared-memory-resident scratch when the largest problem of the batch fits,

@@ -16,7 +16,7 @@
 
 namespace mba {
 
-enum { TRI_OK = 0, TRI_FEW = 1, TRI_BASELINE = 2, TRI_PARALLEL = 3, TRI_BEHIND = 4, TRI_REPROJ = 5 };
+enum { TRI_OK = 0, TRI_FEW = 1, TRI_BASELINE = 2, TRI_PARALLEL = 3, TRI_BEHIND = 4, TRI_REPROJ = 5, TRI_BAD_CAM = 6 };
 
 __device__ __forceinline__ void ray_dir(const double* __restrict__ R, double u, double v, double f, double cx,
                                         double cy, double d[3]) {
@@ -35,7 +35,7 @@ __device__ __forceinline__ void centre(const double* __restrict__ R, const doubl
 
 __global__ void __launch_bounds__(128) triangulate_kernel(
     int n_tracks, const int64_t* __restrict__ off, const int32_t* __restrict__ cam,
-    const double* __restrict__ uv, const double* __restrict__ Rall, const double* __restrict__ tall, double f,
+    const double* __restrict__ uv, int n_cams, const double* __restrict__ Rall, const double* __restrict__ tall, double f,
     double cx, double cy, double max_reproj, double min_angle_deg, int gn_steps, double* __restrict__ X_out,
     int32_t* __restrict__ status, double* __restrict__ err_out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -51,6 +51,11 @@ __global__ void __launch_bounds__(128) triangulate_kernel(
     fail(TRI_FEW);
     return;
   }
+  for (int i = 0; i < n; ++i)   // a camera index outside [0, n_cams) never reads R / t
+    if (cam[o0 + i] < 0 || cam[o0 + i] >= n_cams) {
+      fail(TRI_BAD_CAM);
+      return;
+    }
   // widest-angle pair (degrees(arccos(clip(|d_i . d_j|))), strict > in (i, j) order)
   double best = -1.0;
   int bi = 0, bj = 1;
@@ -184,7 +189,7 @@ extern "C" int32_t mba_triangulate(int32_t n_tracks, const int64_t* obs_off, con
   const int threads = 128;
   const int blocks = (n_tracks + threads - 1) / threads;
   mba::triangulate_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
-      n_tracks, obs_off, cam, uv, R, t, focal, cx, cy, max_reproj_px, min_angle_deg, gn_steps, X, status,
+      n_tracks, obs_off, cam, uv, n_cams, R, t, focal, cx, cy, max_reproj_px, min_angle_deg, gn_steps, X, status,
       mean_err);
   return cudaGetLastError() == cudaSuccess ? MBA_OK : MBA_ERR_CUDA;
 }

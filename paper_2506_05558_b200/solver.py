@@ -103,7 +103,10 @@ def pack_problems(problems) -> HostBatch:
             cam, pt, uv = cam[order], pt[order], uv[order]
         rec, lo = _records(uv, cam.astype(np.int32), pt.astype(np.int32))
         Rs.append(R); ts.append(t); pts.append(X); recs.append(rec); los.append(lo)
-        fixed.append(np.asarray(get(p, "fixed_cams"), dtype=bool).reshape(-1).astype(np.uint8))
+        fc = np.asarray(get(p, "fixed_cams"), dtype=bool).reshape(-1)
+        if len(fc) != n:   # a wrong length would shift every later problem's flags
+            raise ValueError(f"fixed_cams has {len(fc)} entries for {n} cameras")
+        fixed.append(fc.astype(np.uint8))
         n_c.append(n); n_p.append(len(X)); n_o.append(len(uv))
         cx.append(float(get(p, "cx"))); cy.append(float(get(p, "cy"))); foc.append(float(get(p, "focal")))
         of = bool(get(p, "optimize_focal"))

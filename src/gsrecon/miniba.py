@@ -261,6 +261,19 @@ def lm_solve_batch(problems, cfg: LmConfig, precision: str | None = None):
     prm = solver.LmParams.from_cfg(cfg)
     if precision is not None:
         prm.precision = precision
+    problems = list(problems)
+    big = [i for i, p in enumerate(problems) if len(np.asarray(p.R).reshape(-1, 9)) > MAX_FUSED_CAMS]
+    if big:
+        # more cameras than the fused kernel holds: the stage-kernel loop
+        from paper_2506_05558_b200.batch import BatchResult
+        small = [i for i in range(len(problems)) if i not in set(big)]
+        part = lm_solve_batch([problems[i] for i in small], cfg, precision) if small else None
+        res = BatchResult(len(problems), prm.max_iters)
+        for j, i in enumerate(small):
+            res.set(i, part[j])
+        for i in big:
+            res.set(i, _lm_stages(problems[i], cfg, "schur"))
+        return res
     torch = _torch()
     key = torch.cuda.current_device()
     bs = _SOLVERS.get(key)
@@ -272,9 +285,16 @@ def lm_solve_batch(problems, cfg: LmConfig, precision: str | None = None):
     return res
 
 
-def _lm_dense(prob: BaProblem, cfg: LmConfig) -> dict:
-    """The reference loop verbatim in structure, every numerical stage on the
-    device stage kernels, solves by the dense verification path."""
+MAX_FUSED_CAMS = 32   # cameras per problem the fused on-device LM loop holds (mba_solve)
+
+
+def _lm_stages(prob: BaProblem, cfg: LmConfig, method: str = "schur") -> dict:
+    """The reference loop (miniba.py:223-296) driven from the host with every
+    numerical stage on the device stage kernels (residuals, robust weights,
+    blocks, assembly, solve_step). Serves method="dense" (the reference's
+    verification path) and problems with more cameras than the fused kernel
+    holds (MAX_FUSED_CAMS); one host round trip per stage, so it is the slow
+    path."""
     loss = _loss_of(cfg)
     cost_fn = huber_cost if loss == "huber" else cauchy_cost
     w_fn = huber_weights if loss == "huber" else cauchy_weights
@@ -283,6 +303,7 @@ def _lm_dense(prob: BaProblem, cfg: LmConfig) -> dict:
     e = np.linalg.norm(r, axis=1)
     cost = cost_fn(e, cfg.huber_delta)
     costs, accepted, lambdas, evals = [cost], [], [], []
+    status = 0   # MBA_SOLVE_MAX_ITERS / 1 converged / 2 lambda cap, as mba_solve reports
     free = np.flatnonzero(~np.asarray(prob.fixed_cams, dtype=bool))
     for _ in range(cfg.max_iters):
         w = w_fn(e, cfg.huber_delta)
@@ -290,7 +311,7 @@ def _lm_dense(prob: BaProblem, cfg: LmConfig) -> dict:
         blocks = _assemble(prob, w, r, A, F, B)
         lambdas.append(lam)
         try:
-            dc, dp = solve_step(*blocks, lam, "dense")
+            dc, dp = solve_step(*blocks, lam, method)
         except np.linalg.LinAlgError:
             lam = min(lam * cfg.nu, LAMBDA_MAX)
             accepted.append(False)
@@ -322,6 +343,7 @@ def _lm_dense(prob: BaProblem, cfg: LmConfig) -> dict:
             accepted.append(False)
             costs.append(cost)
             if lam >= LAMBDA_MAX:
+                status = 2
                 break
             continue
         lam = max(lam / cfg.nu, 1e-15) if took == 1.0 else min(lam * cfg.nu, LAMBDA_MAX)
@@ -330,10 +352,11 @@ def _lm_dense(prob: BaProblem, cfg: LmConfig) -> dict:
         accepted.append(True)
         costs.append(cost)
         if gain <= 1e-15 * max(cost, 1.0):
+            status = 1
             break
     return dict(costs=np.array(costs), accepted=np.array(accepted, dtype=bool),
                 lambdas=np.array(lambdas), final_rms=float(np.sqrt(np.mean(e ** 2))),
-                mean_err=float(np.mean(e)), evals=np.array(evals, dtype=np.int32))
+                mean_err=float(np.mean(e)), evals=np.array(evals, dtype=np.int32), status=status)
 
 
 def lm_solve(prob: BaProblem, cfg: LmConfig, method: str = "schur") -> dict:
@@ -343,7 +366,7 @@ def lm_solve(prob: BaProblem, cfg: LmConfig, method: str = "schur") -> dict:
     if len(prob.uv) == 0:
         raise ValueError("problem has no residuals")
     if method == "dense":
-        return _lm_dense(prob, cfg)
+        return _lm_stages(prob, cfg, "dense")
     if method != "schur":
         raise ValueError(f"unknown method {method!r}")
     return lm_solve_batch([prob], cfg)[0]
@@ -521,10 +544,14 @@ def match_batch(descriptors: list, pairs, ratio_max: float = 0.95) -> list:
     nn_ba, ok_b = i32(rb), u8(rb)
     d_desc, d_off, d_pairs = _dev(desc), _dev(off), _dev(pairs)
     d_ra, d_rb = _dev(row_a[:-1]), _dev(row_b[:-1])
-    _lib.check(_lib.lib().mba_match_pairs(len(descriptors), ptr(d_desc), ptr(d_off), len(pairs), ptr(d_pairs),
-                                          ptr(d_ra), ptr(d_rb), int(max(sizes.max(), 1)), float(ratio_max),
-                                          ptr(nn_ab), ptr(ok_a), ptr(best_ab), ptr(nn_ba), ptr(ok_b),
-                                          ptr(match_b), ptr(dist), _lib.stream_ptr()),
+    L = _lib.lib()
+    max_rows = int(max(sizes.max(), 1))
+    nws = int(L.mba_match_workspace_bytes(ra, rb, max_rows))
+    ws = _empty((max(nws, 16),), torch.uint8)
+    _lib.check(L.mba_match_pairs(len(descriptors), ptr(d_desc), ptr(d_off), len(pairs), ptr(d_pairs),
+                                 ptr(d_ra), ptr(d_rb), max_rows, float(ratio_max), ptr(nn_ab), ptr(ok_a),
+                                 ptr(best_ab), ptr(nn_ba), ptr(ok_b), ptr(match_b), ptr(dist), ra, rb, ptr(ws),
+                                 ws.numel(), _lib.stream_ptr()),
                "mba_match_pairs")
     mb, dd = _host(match_b), _host(dist)
     out = []
@@ -537,7 +564,8 @@ def match_batch(descriptors: list, pairs, ratio_max: float = 0.95) -> list:
 
 
 TRIANGULATION_FAILURES = {1: "need at least two observations", 2: "baseline angle too small",
-                          3: "parallel rays", 4: "point behind a camera", 5: "mean reprojection too large"}
+                          3: "parallel rays", 4: "point behind a camera", 5: "mean reprojection too large",
+                          6: "camera index out of range"}
 
 
 def triangulate_batch(R: np.ndarray, t: np.ndarray, cam: np.ndarray, pixels: np.ndarray,
@@ -554,6 +582,10 @@ def triangulate_batch(R: np.ndarray, t: np.ndarray, cam: np.ndarray, pixels: np.
     T = len(off) - 1
     if T <= 0:
         return np.zeros((0, 3)), np.zeros(0, np.int32), np.zeros(0)
+    n_cams = len(np.asarray(R).reshape(-1, 9))
+    cam_arr = np.asarray(cam)
+    if len(cam_arr) and (cam_arr.min() < 0 or cam_arr.max() >= n_cams):
+        raise IndexError("camera index out of range")
     dR = _dev(np.asarray(R, np.float64).reshape(-1, 3, 3))
     dt = _dev(np.asarray(t, np.float64).reshape(-1, 3))
     dcam = _dev(np.asarray(cam, np.int32))

@@ -359,3 +359,29 @@ def test_config3_full_batch_on_production_plan(precision, cuda_ok):
         assert dev[i]["status"] in (1, 2)
         assert_parity(dev[i], ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"], R, t, f,
                       label=f"cfg3[{i}]:{precision}")
+
+
+def test_more_than_32_cameras_take_the_stage_kernel_loop(cuda_ok):
+    """The reference lm_solve accepts any camera count; problems beyond the
+    fused kernel's 32 cameras run the stage-kernel LM loop (device stages,
+    host-driven; gsrecon.miniba._lm_stages) and match the oracle."""
+    from gsrecon.config import LmConfig
+    from gsrecon.miniba import BaProblem, MAX_FUSED_CAMS, lm_solve, lm_solve_batch
+    from paper_2506_05558_b200.synth import make_batch
+    p = make_batch(1, n_cams=40, K=3000, seed=51).problem(0)
+    assert len(p["R"]) > MAX_FUSED_CAMS
+    q = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in p.items()}
+    ref = O.lm(q, max_iters=30)
+    prob = BaProblem(**{k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in p.items()})
+    info = lm_solve(prob, LmConfig(max_iters=30))
+    dev = dict(info, R=prob.R, t=prob.t, focal=prob.focal)
+    assert_parity(dev, ref["costs"], ref["accepted"], ref["evals"], ref["lambdas"], q["R"], q["t"], q["focal"],
+                  label="40cams")
+    # mixed batch: the 40-camera problem beside fused-kernel problems
+    small = make_batch(2, n_cams=8, K=1000, seed=52)
+    probs = [BaProblem(**small.problem(0)),
+             BaProblem(**{k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in p.items()}),
+             BaProblem(**small.problem(1))]
+    res = lm_solve_batch(probs, LmConfig(max_iters=30))
+    np.testing.assert_array_equal(res[1]["costs"], info["costs"])
+    assert res[0]["status"] in (0, 1, 2) and res[2]["status"] in (0, 1, 2)

@@ -167,3 +167,14 @@ def test_build_tracks_device_matches_reference(cuda_ok):
     tracks = build_tracks_device(feats)
     flat = np.array([(ti, fr, k, x, y) for ti, tr in enumerate(tracks) for (fr, k, x, y) in tr])
     np.testing.assert_array_equal(flat, z["tracks"])
+
+
+def test_triangulate_batch_rejects_bad_camera_index(cuda_ok):
+    from gsrecon import miniba as M
+    from gsrecon.scene import CameraIntrinsics
+    z = np.load(f"{GOLDEN}/triangulate.npz")
+    intr = CameraIntrinsics(float(z["focal"]), float(z["cx"]), float(z["cy"]), 640, 480)
+    cam = z["cam"].copy()
+    cam[3] = len(z["R"])
+    with pytest.raises(IndexError):
+        M.triangulate_batch(z["R"], z["t"], cam, z["uv"], z["obs_off"], intr)

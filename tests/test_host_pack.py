@@ -134,3 +134,11 @@ def test_dict_problems_are_accepted():
     dicts = [b.problem(i) for i in range(3)]
     hb, (co, po, oo), lay, buf, ret = _gather(dicts)
     assert ret[3] == -1 and int(oo[-1]) == int(b.obs_off[-1])
+
+
+def test_pack_problems_checks_fixed_cams_length():
+    b = make_batch(2, n_cams=4, K=300, seed=5)
+    ps = [b.problem(i) for i in range(2)]
+    ps[0]["fixed_cams"] = ps[0]["fixed_cams"][:3]
+    with pytest.raises(ValueError, match="fixed_cams"):
+        solver.pack_problems(ps)
