@@ -95,6 +95,24 @@ def main():
                    "ok": bool(rel.max() <= 1e-9)},
     }
     line["speedup_vs_cpu_1core"] = line["device"]["pose_iters_per_s"] / line["cpu_oracle"]["pose_iters_per_s"]
+    # roofline (SURVEY 8d counts one pass over the correspondences per
+    # evaluation: 40 B each -- X 24 + uv 16 -- for the initial cost, and per
+    # iteration the linearisation and the trial cost)
+    try:
+        peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        kind = "measured"
+    except OSError:
+        peak, kind = 6650.0, "fallback"
+    passes = 1 + 2 * it
+    pass_bytes = 40.0 * B * M * passes
+    in_bytes = 40.0 * B * M
+    flops = B * M * (passes * 60.0 + it * 110.0)   # ~60 flop per residual, ~110 per Jacobian + normal-eq update
+    s = dev_ms / 1e3
+    line["roofline"] = {"bytes_model": "40 B per correspondence per pass, %d passes" % passes,
+                        "achieved_pass_gbs": pass_bytes / s / 1e9, "inputs_once_gbs": in_bytes / s / 1e9,
+                        "peak_gbs": peak, "peak_kind": kind, "frac_pass": pass_bytes / s / 1e9 / peak,
+                        "fp64_tflops": flops / s / 1e12, "fp64_peak_tflops": 37.22,
+                        "inputs_bytes": in_bytes, "larger_than_l2": in_bytes > 126 * 2 ** 20}
     print(json.dumps(line))
 
 

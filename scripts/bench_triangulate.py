@@ -34,6 +34,13 @@ def make_tracks(T, n_cams=12, seed=3):
     return Rs, ts, cam, uv, off, (f, cx, cy)
 
 
+def _peak():
+    try:
+        return json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except OSError:
+        return 6650.0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tracks", type=int, default=1_000_000)
@@ -87,6 +94,10 @@ def main():
                    "gn_steps": 3, "data": "synthetic, 0.5 px noise"},
         "device": {"ms_per_call": ms, "tracks_per_s": T / (ms / 1e3),
                    "hbm_gbs_algorithmic": obs_bytes / (ms / 1e3) / 1e9, "kernel": "mba_triangulate"},
+        "roofline": {"bytes_per_launch": float(obs_bytes), "achieved_gbs": obs_bytes / (ms / 1e3) / 1e9,
+                     "peak_gbs": _peak(), "frac": obs_bytes / (ms / 1e3) / 1e9 / _peak(),
+                     "larger_than_l2": bool(obs_bytes > 126 * 2 ** 20),
+                     "bytes_model": "per observation cam 4 + uv 16 B; per track offset 8, X 24, status 4, err 8 B"},
         "cpu_oracle": {"tracks": n, "seconds": t_cpu, "tracks_per_s": n / t_cpu, "cores": 1,
                        "kind": "port (oracle/miniba_oracle.triangulate, numpy)"},
         "parity": {"tracks": n, "status_agree": agree, "max_abs_X_diff": worst,

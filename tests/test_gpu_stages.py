@@ -61,10 +61,18 @@ def test_pose_lm_matches_reference(cuda_ok):
     z = np.load(f"{GOLDEN}/pose_lm.npz")
     intr = CameraIntrinsics(float(z["focal"]), float(z["cx"]), float(z["cy"]), 640, 480)
     R, t, c = M.pose_lm(z["R0"], z["t0"], z["X"], z["uv"], intr, int(z["iters"]), LmConfig())
-    # accept decisions are discrete: compare per hypothesis, allow roundoff-level cost
-    np.testing.assert_allclose(c, z["cost_out"], rtol=1e-6, atol=1e-9)
-    agree = np.abs(t - z["t_out"]).max(axis=1) < 1e-6
-    assert agree.mean() > 0.98
+    # Every hypothesis: same accept decisions (no accept margin in this batch is
+    # below 2.8e-4 relative), final cost to 1e-12. Poses agree to 1e-9 except
+    # the two hypotheses enumerated below, whose last accepted step solves a
+    # normal matrix with cond(H) = 4.1e6 (hyp 3) / 1.7e7 (hyp 140): Huber
+    # outliers leave a flat valley, the fp64 step along it depends on the
+    # summation order, and t lands 1.3e-6 / 2.0e-5 apart at costs equal to
+    # 1e-14 (scripts/pose_diag.py, profiles/round2_pose_diag.json).
+    ILL_CONDITIONED = {3: 1e-5, 140: 1e-4}
+    np.testing.assert_allclose(c, z["cost_out"], rtol=1e-12)
+    dt = np.abs(t - z["t_out"]).max(axis=1)
+    for b in range(len(dt)):
+        assert dt[b] <= ILL_CONDITIONED.get(b, 1e-9), (b, dt[b])
     R, t, c = M.pose_lm(z["Rf0"], z["tf0"], z["Xf"], z["uvf"], intr, int(z["iters_f"]), LmConfig())
     np.testing.assert_allclose(c, z["costf_out"], rtol=1e-9)
     np.testing.assert_allclose(t, z["tf_out"], rtol=1e-7, atol=1e-10)
