@@ -329,8 +329,11 @@ struct GridBufs {
   static __host__ __device__ size_t oPart(int G, int64_t chunks) {   // T[chunks][kUcamStride]
     return align16(oChunk(G) + 8 * (size_t)chunks);
   }
+  static __host__ __device__ size_t oSeg(int G, int64_t chunks) {   // int[G * warps][MAXC]
+    return align16(oPart(G, chunks) + sizeof(T) * kUcamStride * (size_t)chunks);
+  }
   static __host__ __device__ size_t bytes(int G, int64_t chunks) {
-    return oPart(G, chunks) + sizeof(T) * kUcamStride * (size_t)chunks;
+    return oSeg(G, chunks) + 4 * (size_t)G * (kThreads / 32) * MAXC;
   }
 };
 
@@ -476,7 +479,56 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     grid_sum(&fv, 1);
     if (tid == 0) s_flag = fv != 0.0;
   }
-  // camera-major permutation: warp per camera, two ballot sweeps
+  // camera-major permutation
+  if constexpr (GRID) {
+    // cooperative mode: every warp owns a contiguous segment of the
+    // observations; per-segment camera counts, a per-camera scan over the
+    // segments, then each warp scatters its segment in order (one warp per
+    // camera scanning all K observations took ~2 ms at K = 200k)
+    int* seg = (int*)(P.grid + GB::oSeg(nranks, P.grid_chunks));
+    const int seg_len = (K + gwarps - 1) / gwarps;
+    const int s0 = gwid * seg_len, s1 = min(K, s0 + seg_len);
+    const unsigned lt = (1u << lane) - 1u;
+    int my_cnt = 0;   // lane c: observations of camera c in this segment
+    for (int k0 = s0; k0 < s1; k0 += 32) {
+      const int k = k0 + lane;
+      const int cl = k < s1 ? obs_cam(obs, k) : -1;
+      for (int c = 0; c < n; ++c) {
+        const unsigned m = __ballot_sync(0xffffffffu, cl == c);
+        if (lane == c) my_cnt += __popc(m);
+      }
+    }
+    if (lane < n) seg[gwid * n + lane] = my_cnt;
+    gsync();
+    for (int c = gwid; c < n; c += gwarps) {   // exclusive scan over segments, per camera
+      int carry = 0;
+      for (int s_ = 0; s_ < gwarps; s_ += 32) {
+        const int v = s_ + lane < gwarps ? seg[(s_ + lane) * n + c] : 0;
+        const int inc = warp_excl_scan(v, lane) + v;
+        if (s_ + lane < gwarps) seg[(s_ + lane) * n + c] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) gcnt[c + 1] = carry;
+    }
+    gsync();
+    if (tid == 0) {
+      sm.cam_ptr[0] = 0;
+      for (int c = 0; c < n; ++c) sm.cam_ptr[c + 1] = sm.cam_ptr[c] + gcnt[c + 1];
+    }
+    __syncthreads();
+    int my_base = lane < n ? sm.cam_ptr[lane] + seg[gwid * n + lane] : 0;
+    for (int k0 = s0; k0 < s1; k0 += 32) {
+      const int k = k0 + lane;
+      const int cl = k < s1 ? obs_cam(obs, k) : -1;
+      for (int c = 0; c < n; ++c) {
+        const unsigned m = __ballot_sync(0xffffffffu, cl == c);
+        const int bc = __shfl_sync(0xffffffffu, my_base, c);
+        if (cl == c) perm[bc + __popc(m & lt)] = k;
+        if (lane == c) my_base += __popc(m);
+      }
+    }
+    gsync();
+  } else {
   for (int c = gwid; c < n; c += gwarps) {
     int cnt = 0;
     for (int k0 = 0; k0 < K; k0 += 32) {
@@ -505,6 +557,7 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     }
   }
   gsync();
+  }
   const int nf = s_nf, C = s_C, FI = C - 1;
   const int nb = opt_pts ? nf * (nf + 1) / 2 : 0;
   // co-observation pair lists per camera block (a <= b): count, scan, fill
