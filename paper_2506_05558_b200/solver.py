@@ -334,105 +334,3 @@ def fetch(sol: Solution, b: int = 0) -> dict:
                 evals=sol.evals[b, :n].cpu().numpy().astype(np.int32),
                 final_rms=float(np.sqrt(st[2] / K)), mean_err=float(st[1] / K),
                 status=int(sol.status[b].item()))
-
-
-# ---------------------------------------------------------------------------
-# host-to-host batched solve with copy/compute overlap (the end-to-end path)
-
-def split_host_batch(hb: HostBatch, n_chunks: int):
-    """Contiguous problem ranges of a host batch as self-contained HostBatch
-    views (offset arrays rebased; data arrays are views, no copies)."""
-    B = hb.n_problems
-    n_chunks = max(1, min(n_chunks, B))
-    cuts = [B * i // n_chunks for i in range(n_chunks + 1)]
-    parts = []
-    for a, b in zip(cuts[:-1], cuts[1:]):
-        c0, c1 = hb.cam_off[a], hb.cam_off[b]
-        p0, p1 = hb.pt_off[a], hb.pt_off[b]
-        o0, o1 = hb.obs_off[a], hb.obs_off[b]
-        parts.append(HostBatch(
-            cam_off=hb.cam_off[a:b + 1] - c0, pt_off=hb.pt_off[a:b + 1] - p0,
-            obs_off=hb.obs_off[a:b + 1] - o0, obs=hb.obs[o0:o1],
-            obs_lo=None if hb.obs_lo is None else hb.obs_lo[o0:o1], fixed=hb.fixed[c0:c1],
-            cx=hb.cx[a:b], cy=hb.cy[a:b], flags=hb.flags[a:b], R=hb.R[c0:c1], t=hb.t[c0:c1],
-            focal=hb.focal[a:b], points=hb.points[p0:p1], max_pairs=hb.max_pairs,
-            max_track=hb.max_track))
-    return parts, cuts
-
-
-class PipelinedSolver:
-    """End-to-end solve of a host batch: H2D of chunk i+1 overlaps the solve
-    of chunk i on a second stream; each chunk's solution (R, t, focal, points,
-    final stats, n_iters, status) is copied back to pinned host memory.
-    Chunk solves alternate between two compute streams (each chunk has its own
-    workspace), so the next chunk's problems fill the SMs the previous chunk's
-    last problems leave idle instead of waiting for its tail."""
-
-    OUT = ("R", "t", "focal", "points", "final_stats", "n_iters", "status")
-
-    def __init__(self, hb: HostBatch, prm: LmParams, n_chunks: int = 4):
-        torch = _lib.torch_cuda()
-        self.prm = prm
-        self.parts, self.cuts = split_host_batch(hb, n_chunks)
-        self.pinned = [pin(p) for p in self.parts]
-        self.copy = torch.cuda.Stream()      # host -> device
-        self.compute = torch.cuda.Stream()
-        self.compute2 = torch.cuda.Stream()
-        self.back = torch.cuda.Stream()      # device -> host (own stream: a chunk's read-back
-        #                                      must not hold up the next chunk's upload)
-        self.dev = [to_device(p, pinned=self.pinned[i]) for i, p in enumerate(self.parts)]
-        torch.cuda.synchronize()
-        self.sols = [Solution(d, prm.max_iters) for d in self.dev]
-        self.ws = [torch.empty(max(workspace_bytes(d, prm), 16), dtype=torch.uint8, device=d.obs.device)
-                   for d in self.dev]
-        self.host = [{k: torch.empty(getattr(s, k).shape, dtype=getattr(s, k).dtype, pin_memory=True)
-                      for k in self.OUT} for s in self.sols]
-        self.h2d_bytes = sum(d.h2d_bytes for d in self.dev)
-        self.d2h_bytes = sum(v.numel() * v.element_size() for h in self.host for v in h.values())
-
-    def run(self):
-        """Enqueue H2D -> solve -> D2H for every chunk (asynchronous).
-
-        Consecutive runs pipeline per chunk: run n+1's upload of chunk i waits
-        only for run n's solve of chunk i (it overwrites that chunk's device
-        inputs) and its solve of chunk i for run n's read-back of chunk i (it
-        overwrites the outputs), so the next run's first uploads overlap this
-        run's last solves instead of waiting for the whole run."""
-        torch = _lib.torch_cuda()
-        fields = _INPUT_FIELDS
-        if not hasattr(self, "_solved"):
-            self._solved = [None] * len(self.dev)
-            self._read = [None] * len(self.dev)
-        for i, (d, src) in enumerate(zip(self.dev, self.pinned)):
-            if self._solved[i] is not None:
-                self.copy.wait_event(self._solved[i])
-            with torch.cuda.stream(self.copy):
-                for k in fields:
-                    if src[k] is not None:
-                        getattr(d, k).copy_(src[k], non_blocking=True)
-                h2d = torch.cuda.Event()
-                h2d.record(self.copy)
-            cs = self.compute if i % 2 == 0 else self.compute2
-            cs.wait_event(h2d)
-            if self._read[i] is not None:
-                cs.wait_event(self._read[i])
-            with torch.cuda.stream(cs):
-                solve(d, self.prm, self.sols[i], ws=self.ws[i])
-                done = torch.cuda.Event()
-                done.record(cs)
-            self._solved[i] = done
-            self.back.wait_event(done)
-            with torch.cuda.stream(self.back):
-                for k in self.OUT:
-                    self.host[i][k].copy_(getattr(self.sols[i], k), non_blocking=True)
-                rd = torch.cuda.Event()
-                rd.record(self.back)
-            self._read[i] = rd
-        return self
-
-    def wait(self):
-        """Make the current stream wait for every copy and solve of run()."""
-        torch = _lib.torch_cuda()
-        cur = torch.cuda.current_stream()
-        for s_ in (self.copy, self.compute, self.compute2, self.back):
-            cur.wait_stream(s_)

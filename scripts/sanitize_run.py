@@ -1,6 +1,8 @@
 """Small workloads for compute-sanitizer: the cluster-resident solver (f64 and
-mixed, R = 1, a 16-CTA and a 10-CTA cluster, overflow re-solve), pose LM, triangulation
-and matching."""
+mixed, R = 1, a 16-CTA and a 10-CTA cluster, overflow re-solve), the
+cooperative grid solver (12 cameras), the device pack / sort kernel through
+lm_solve_batch (shuffled observations), the bootstrap schedule, pose LM,
+triangulation and matching."""
 import os
 import sys
 
@@ -27,8 +29,35 @@ def main():
     os.environ["MBA_V4_ARENA_CAP"] = "20000"
     run_device(probs[:1], dict(max_iters=4), "f64", "auto")  # overflow -> CTA kernel
     del os.environ["MBA_V4_ARENA_CAP"]
+    grid = make_batch(1, n_cams=12, K=6000, seed=6).problem(0)
+    run_device([grid], dict(max_iters=3), "f64", "grid")     # cooperative grid kernel
     from gsrecon import miniba as M
+    from gsrecon.config import CaptureConfig, LmConfig
     from gsrecon.scene import CameraIntrinsics
+    # list path: native gather, device stable sort of shuffled observations
+    ps = []
+    for i in range(3):
+        p = b.problem(i)
+        perm = np.random.default_rng(i).permutation(len(p["uv"]))
+        for k in ("cam_idx", "pt_idx", "uv"):
+            p[k] = p[k][perm]
+        ps.append(M.BaProblem(**p))
+    M.lm_solve_batch(ps, LmConfig(max_iters=6))
+    # bootstrap schedule (solve, filter, compaction, solve, gauge) on one window
+    bz = np.load(os.path.join(REPO, "tests", "golden", "bootstrap_seed0.npz"))
+    feats, o = [], 0
+    for c in bz["counts"]:
+        feats.append((bz["keypoints"][o:o + c], bz["ids"][o:o + c]))
+        o += c
+
+    def exact(fa, fb):
+        _, ia, ib = np.intersect1d(fa[1], fb[1], assume_unique=True, return_indices=True)
+        return ia.astype(np.int64), ib.astype(np.int64), np.zeros(len(ia))
+    cfg = CaptureConfig()
+    cfg.bootstrap_iters = 10
+    bintr = CameraIntrinsics(float(bz["focal"]), float(bz["cx"]), float(bz["cy"]), int(bz["width"]),
+                             int(bz["height"]))
+    M.bootstrap_batch([feats], [bintr], cfg, matcher=exact)
     z = np.load(os.path.join(REPO, "tests", "golden", "triangulate.npz"))
     intr = CameraIntrinsics(float(z["focal"]), float(z["cx"]), float(z["cy"]), 640, 480)
     M.triangulate_batch(z["R"], z["t"], z["cam"], z["uv"], z["obs_off"][:101], intr)

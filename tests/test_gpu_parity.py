@@ -245,30 +245,6 @@ def test_plan_overflow_is_resolved_by_cta_kernel(cuda_ok, monkeypatch):
                           probs[i]["R"], probs[i]["t"], probs[i]["focal"], label=f"overflow[{i}]")
 
 
-def test_pipelined_host_to_host_solver_matches_device_solve(cuda_ok):
-    """The e2e path (chunked H2D -> mba_solve -> D2H on three streams, run
-    twice back to back) returns exactly the device solve's results."""
-    import torch
-    from paper_2506_05558_b200 import solver
-    from paper_2506_05558_b200.synth import make_batch
-    b = make_batch(40, n_cams=8, K=2000, seed=31)
-    hb = solver.pack_synth(b)
-    prm = solver.LmParams(max_iters=200, precision="f64")
-    sol = solver.solve(solver.to_device(hb), prm)
-    torch.cuda.synchronize()
-    ps = solver.PipelinedSolver(hb, prm, n_chunks=4)
-    for _ in range(2):
-        ps.run()
-    ps.wait()
-    torch.cuda.synchronize()
-    for i, (a, z) in enumerate(zip(ps.cuts[:-1], ps.cuts[1:])):
-        h = ps.host[i]
-        np.testing.assert_array_equal(h["final_stats"].numpy(), sol.final_stats[a:z].cpu().numpy())
-        np.testing.assert_array_equal(h["n_iters"].numpy(), sol.n_iters[a:z].cpu().numpy())
-        p0, p1 = hb.pt_off[a], hb.pt_off[z]
-        np.testing.assert_array_equal(h["points"].numpy(), sol.points[p0:p1].cpu().numpy())
-
-
 def test_heterogeneous_batch_cluster_kernel(cuda_ok):
     """One batch mixing camera counts (3..8), sizes (K 300..3000), free /
     fixed focal, fixed points and two fixed cameras: every problem matches the
