@@ -115,20 +115,21 @@ typedef struct {
 } MbaOutputs;
 
 /* Device-side packing of raw per-problem observation arrays (BaProblem
- * cam_idx / pt_idx / uv, miniba.py:65-83, uploaded as int32 / int32 / float64
- * back to back per problem) into the MbaObs records mba_solve consumes:
- * stable point-major order within each problem (numpy argsort(kind="stable")
- * of pt_idx), u/v rounded to float, and -- when out_lo is not NULL -- the
- * low-order float2 stream uv - float(uv). Replaces the host-side sort of the
- * producers' track-major (miniba.py:762-770) or camera-major
- * (smoke_miniba.py:50-55) arrays. Problems with an out-of-range index are
- * written unsorted; mba_solve then reports them malformed (status -1).
- * workspace: >= mba_pack_obs_workspace_bytes(total points) bytes. */
+ * cam_idx / pt_idx / uv, miniba.py:65-83, uploaded back to back per problem as
+ * int32 / int32 / uv rounded to float32, plus -- only when some pixel is not
+ * fp32-representable -- the low-order float32 residual uv_lo = uv - float(uv))
+ * into the MbaObs records mba_solve consumes: stable point-major order within
+ * each problem (numpy argsort(kind="stable") of pt_idx) and, when out_lo and
+ * uv_lo are not NULL, the low-order stream in the same order. Replaces the
+ * host-side sort of the producers' track-major (miniba.py:762-770) or
+ * camera-major (smoke_miniba.py:50-55) arrays. Problems with an out-of-range
+ * index are written unsorted; mba_solve then reports them malformed
+ * (status -1). workspace: >= mba_pack_obs_workspace_bytes(total points) bytes. */
 size_t mba_pack_obs_workspace_bytes(int64_t total_points);
 int32_t mba_pack_obs(int32_t n_problems, const int64_t* obs_off, const int64_t* pt_off,
-                     const int64_t* cam_off, const int32_t* cam, const int32_t* pt, const double* uv,
-                     MbaObs* out, float* out_lo, void* workspace, size_t workspace_bytes,
-                     void* stream);
+                     const int64_t* cam_off, const int32_t* cam, const int32_t* pt, const float* uv,
+                     const float* uv_lo, MbaObs* out, float* out_lo, void* workspace,
+                     size_t workspace_bytes, void* stream);
 
 /* The bootstrap schedule around lm_solve (miniba.py:782-805, run_schedule) as
  * one device sequence over a batch of independent problems, no host round
@@ -148,6 +149,18 @@ int32_t mba_bootstrap_schedule(const MbaBatchDesc* desc, const MbaLmConfig* cfg1
                                int64_t* obs_off2, int64_t* n_kept, uint8_t* pt_alive,
                                double* gauge_scale, void* workspace, size_t workspace_bytes,
                                void* stream);
+
+/* Packs the per-problem LM traces of an mba_solve (MbaOutputs costs /
+ * lambdas / accepted / evals, max_iters wide) back to back before a read-back:
+ * trace_off[b] = sum of n_iters over problems before b (n_problems + 1
+ * entries); problem b's n_iters lambdas / accepted / evals land at
+ * trace_off[b] and its n_iters + 1 costs at trace_off[b] + b. Output buffers
+ * are sized for the worst case (n_problems * max_iters, costs + n_problems). */
+int32_t mba_compact_traces(int32_t n_problems, int32_t max_iters, const int32_t* n_iters,
+                           const double* costs, const double* lambdas, const uint8_t* accepted,
+                           const uint8_t* evals, int64_t* trace_off, double* costs_out,
+                           double* lambdas_out, uint8_t* accepted_out, uint8_t* evals_out,
+                           void* stream);
 
 int32_t mba_abi_version(void);
 

@@ -90,7 +90,9 @@ def lib():
     L.mba_pack_obs_workspace_bytes.restype = sz
     L.mba_pack_obs_workspace_bytes.argtypes = [i64]
     L.mba_pack_obs.restype = i32
-    L.mba_pack_obs.argtypes = [i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, sz, _vp]
+    L.mba_pack_obs.argtypes = [i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, sz, _vp]
+    L.mba_compact_traces.restype = i32
+    L.mba_compact_traces.argtypes = [i32, i32] + [_vp] * 10 + [_vp]
     L.mba_bootstrap_workspace_bytes.restype = sz
     L.mba_bootstrap_workspace_bytes.argtypes = [ct.POINTER(MbaBatchDesc), ct.POINTER(MbaLmConfig)]
     L.mba_bootstrap_schedule.restype = i32
@@ -106,7 +108,8 @@ def lib():
 EXPORTED = ("mba_abi_version", "mba_workspace_bytes", "mba_solve", "mba_solve_plan", "mba_solve_launches", "mba_residuals", "mba_robust",
             "mba_blocks", "mba_assemble", "mba_solve_step_scratch_bytes", "mba_solve_step",
             "mba_pose_lm", "mba_triangulate", "mba_match_pairs", "mba_match_workspace_bytes", "mba_pack_obs_workspace_bytes",
-            "mba_pack_obs", "mba_bootstrap_workspace_bytes", "mba_bootstrap_schedule")
+            "mba_pack_obs", "mba_bootstrap_workspace_bytes", "mba_bootstrap_schedule",
+            "mba_compact_traces")
 
 
 def check(rc, what):

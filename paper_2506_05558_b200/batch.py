@@ -12,7 +12,7 @@ hypotheses is a Python list of such objects, so the end-to-end path is:
     --(D2H, read-back stream)--> pinned --(threaded in-place write-back)-->
     the callers' R / t / points arrays (+ focal rebound), lazy info dicts.
 
-The batch is cut into chunks that flow through a three-slot ring, so the
+The batch is cut into chunks that flow through a four-slot ring, so the
 host walk / gather of chunk i+1 and the write-back of chunk i-1 overlap the
 device work of chunk i, and consecutive chunk solves alternate between two
 compute streams (the next chunk's problems fill the SMs the previous chunk's
@@ -57,8 +57,8 @@ def default_threads():
 _REGIONS = (("cam_off", 0, 0, 0, 8, 8), ("pt_off", 0, 0, 0, 8, 8), ("obs_off", 0, 0, 0, 8, 8),
             ("cx", 0, 0, 0, 8, 0), ("cy", 0, 0, 0, 8, 0), ("focal", 0, 0, 0, 8, 0),
             ("R", 72, 0, 0, 0, 0), ("t", 24, 0, 0, 0, 0), ("points", 0, 24, 0, 0, 0),
-            ("uv", 0, 0, 16, 0, 0), ("cam", 0, 0, 4, 0, 0), ("pt", 0, 0, 4, 0, 0),
-            ("fixed", 1, 0, 0, 0, 0), ("flags", 0, 0, 0, 1, 0))
+            ("uv", 0, 0, 8, 0, 0), ("cam", 0, 0, 4, 0, 0), ("pt", 0, 0, 4, 0, 0),
+            ("fixed", 1, 0, 0, 0, 0), ("flags", 0, 0, 0, 1, 0), ("uv_lo", 0, 0, 8, 0, 0))
 
 
 def layout(n_cams, n_pts, n_obs, m):
@@ -68,23 +68,28 @@ def layout(n_cams, n_pts, n_obs, m):
     for name, pc, pp, po, pb, extra in _REGIONS:
         off[name] = pos
         pos += (pc * n_cams + pp * n_pts + po * n_obs + pb * m + extra + 15) & ~15
+    # the trailing low-order uv stream is uploaded only when a chunk needs it
     return off, pos
 
 
 class BatchResult:
     """Per-problem LM info of a batched solve, materialised lazily: item b is
     the dict `lm_solve` returns (costs, accepted, lambdas, final_rms, mean_err;
-    plus evals and status), miniba.py:294-296."""
+    plus evals and status), miniba.py:294-296. The traces are held ragged
+    (only each problem's n_iters entries, as the device packed them)."""
 
     def __init__(self, B, max_iters):
-        w = max(max_iters, 1)
-        self.costs = np.empty((B, max_iters + 1))
-        self.lambdas = np.empty((B, w))
-        self.accepted = np.empty((B, w), np.uint8)
-        self.evals = np.empty((B, w), np.uint8)
-        self.n_iters = np.empty(B, np.int32)
-        self.status = np.empty(B, np.int32)
-        self.final_stats = np.empty((B, 4))
+        self.max_iters = max_iters
+        self.n_iters = np.zeros(B, np.int32)
+        self.status = np.zeros(B, np.int32)
+        self.final_stats = np.zeros((B, 4))
+        self._starts = []       # first problem of each stored chunk
+        self._chunks = []       # (lo, hi, off, costs, lambdas, accepted, evals)
+        self._override = {}
+
+    def add_chunk(self, lo, hi, off, costs, lambdas, accepted, evals):
+        self._starts.append(lo)
+        self._chunks.append((lo, hi, off, costs, lambdas, accepted, evals))
 
     def __len__(self):
         return len(self.n_iters)
@@ -96,12 +101,17 @@ class BatchResult:
             b += len(self)
         if not 0 <= b < len(self):
             raise IndexError(b)
-        n = int(self.n_iters[b])
+        if b in self._override:
+            return dict(self._override[b])
+        import bisect
+        lo, hi, off, c, lam, acc, ev = self._chunks[bisect.bisect_right(self._starts, b) - 1]
+        j = b - lo
+        o0, o1 = int(off[j]), int(off[j + 1])
         st = self.final_stats[b]
         K = max(st[3], 1.0)
-        return dict(costs=self.costs[b, :n + 1].copy(), accepted=self.accepted[b, :n].astype(bool),
-                    lambdas=self.lambdas[b, :n].copy(), final_rms=float(np.sqrt(st[2] / K)),
-                    mean_err=float(st[1] / K), evals=self.evals[b, :n].astype(np.int32),
+        return dict(costs=c[o0 + j:o1 + j + 1].copy(), accepted=acc[o0:o1].astype(bool),
+                    lambdas=lam[o0:o1].copy(), final_rms=float(np.sqrt(st[2] / K)),
+                    mean_err=float(st[1] / K), evals=ev[o0:o1].astype(np.int32),
                     status=int(self.status[b]))
 
     def __iter__(self):
@@ -110,19 +120,19 @@ class BatchResult:
 
     def set(self, b, info):
         """Store problem b's info dict (problems solved outside the batch)."""
-        n = len(info["accepted"])
-        self.costs[b, :n + 1] = info["costs"]
-        self.accepted[b, :n] = info["accepted"]
-        self.lambdas[b, :n] = info["lambdas"]
-        self.evals[b, :n] = info.get("evals", np.zeros(n))
-        self.n_iters[b] = n
-        self.status[b] = info.get("status", -3)
-        K = 1.0
-        self.final_stats[b] = (info["costs"][-1], info["mean_err"] * K, info["final_rms"] ** 2 * K, K)
+        d = dict(info)
+        d.setdefault("evals", np.zeros(len(d["accepted"]), np.int32))
+        d.setdefault("status", -3)
+        self._override[b] = d
+        self.n_iters[b] = len(d["accepted"])
+        self.status[b] = d["status"]
+        self.final_stats[b] = (d["costs"][-1], d["mean_err"], d["final_rms"] ** 2, 1.0)
 
 
-_OUT = ("R", "t", "focal", "points", "costs", "lambdas", "accepted", "evals", "n_iters", "status",
-        "final_stats")
+# fixed-size outputs read back per chunk; the traces are packed on the device
+# first (mba_compact_traces) and read back ragged
+_OUT = ("R", "t", "focal", "points", "n_iters", "status", "final_stats", "trace_off")
+_TRACES = ("costs", "lambdas", "accepted", "evals")
 
 
 class _Slot:
@@ -154,12 +164,16 @@ class _Slot:
         self.lo = self._grow(self.lo, 8 * K, torch, device=self.device, **u8)
         self.pack_ws = self._grow(self.pack_ws, 4 * max(P, 1), torch, device=self.device, **u8)
         w = max(max_iters, 1)
-        shapes = dict(R=(C * 9, torch.float64), t=(C * 3, torch.float64), focal=(B, torch.float64),
-                      points=(P * 3, torch.float64), costs=(B * (max_iters + 1), torch.float64),
-                      lambdas=(B * w, torch.float64), accepted=(B * w, torch.uint8),
-                      evals=(B * w, torch.uint8), n_iters=(B, torch.int32), status=(B, torch.int32),
-                      final_stats=(B * 4, torch.float64))
-        for k, (n, dt) in shapes.items():
+        f64, u8_, i32 = torch.float64, torch.uint8, torch.int32
+        dev_only = dict(costs=(B * (max_iters + 1), f64), lambdas=(B * w, f64), accepted=(B * w, u8_),
+                        evals=(B * w, u8_))
+        both = dict(R=(C * 9, f64), t=(C * 3, f64), focal=(B, f64), points=(P * 3, f64), n_iters=(B, i32),
+                    status=(B, i32), final_stats=(B * 4, f64), trace_off=(B + 1, torch.int64),
+                    c_costs=(B * (max_iters + 1), f64), c_lambdas=(B * w, f64), c_accepted=(B * w, u8_),
+                    c_evals=(B * w, u8_))
+        for k, (n, dt) in dev_only.items():
+            self.out_d[k] = self._grow(self.out_d.get(k), n, torch, dtype=dt, device=self.device)
+        for k, (n, dt) in both.items():
             self.out_d[k] = self._grow(self.out_d.get(k), n, torch, dtype=dt, device=self.device)
             self.out_h[k] = self._grow(self.out_h.get(k), n, torch, dtype=dt, pin_memory=True)
 
@@ -173,7 +187,7 @@ class BatchSolver:
     points written in place when the arrays are writable float64, rebound
     otherwise; focal rebound) and returns a `BatchResult`."""
 
-    def __init__(self, prm, n_chunks=8, min_chunk=512, threads=None, device=None):
+    def __init__(self, prm, n_chunks=16, min_chunk=512, threads=None, device=None, ring=4):
         torch = _lib.torch_cuda()
         self.torch = torch
         self.prm = prm
@@ -184,13 +198,29 @@ class BatchSolver:
         self.copy = torch.cuda.Stream(self.device)
         self.compute = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)]
         self.back = torch.cuda.Stream(self.device)
-        self.slots = [_Slot(torch, self.device) for _ in range(3)]
+        self.trace_back = torch.cuda.Stream(self.device)   # packed-trace read-backs (own queue: the
+        #                                                    read-back stream holds later chunks' copies)
+        self.slots = [_Slot(torch, self.device) for _ in range(ring)]
         self.h2d_bytes = self.d2h_bytes = 0
         self.launches = 0
 
     def chunks(self, B):
+        """Chunk boundaries. With enough chunks the first and last two are
+        smaller (weights 1/4, 1/2 ... 1/2, 1/4): the device starts after a
+        short first host gather, and the last read-back + write-back, which
+        nothing overlaps, is short too."""
         n = max(1, min(self.n_chunks, B // max(self.min_chunk, 1)))
-        return [B * i // n for i in range(n + 1)]
+        w = [1.0] * n
+        if n >= 6:
+            w[0] = w[-1] = 0.25
+            w[1] = w[-2] = 0.5
+        tot = sum(w)
+        cuts, acc = [0], 0.0
+        for x in w:
+            acc += x
+            cuts.append(int(round(B * acc / tot)))
+        cuts[-1] = B
+        return sorted(set(cuts))
 
     def solve(self, problems) -> BatchResult:
         torch, prm, H = self.torch, self.prm, host_module()
@@ -203,13 +233,23 @@ class BatchSolver:
         pending = []
         self.h2d_bytes = self.d2h_bytes = 0
         self.launches = 0
+        self.host_s = {}   # host-side seconds per stage of the last call (diagnostics)
         L = _lib.lib()
+        import time
+        clock = time.perf_counter
+
+        def tick(name, t0):
+            self.host_s[name] = self.host_s.get(name, 0.0) + clock() - t0
         for ci, (lo, hi) in enumerate(zip(cuts[:-1], cuts[1:])):
-            slot = self.slots[ci % 3]
-            # a slot is reused three chunks later: its previous chunk must be
+            ring = len(self.slots)
+            slot = self.slots[ci % ring]
+            # a slot is reused `ring` chunks later: its previous chunk must be
             # written back (host) before the pinned buffers are overwritten
-            while pending and pending[0][0] <= ci - 3:
+            t0 = clock()
+            while pending and pending[0][0] <= ci - ring:
                 self._finish(pending.pop(0), res)
+            tick("finish", t0)
+            t0 = clock()
             chunk = problems[lo:hi]
             try:
                 batch = H.Batch(chunk)
@@ -224,9 +264,20 @@ class BatchSolver:
             C, P, K = int(co[-1]), int(po[-1]), int(oo[-1])
             lay, nbytes = layout(C, P, K, m)
             slot.ensure(nbytes, K, P, C, m, prm.max_iters)
+            tick("walk", t0)
+            t0 = clock()
             if slot.h2d is not None:
                 slot.h2d.synchronize()
-            any_lo, max_pairs, max_track, bad = batch.gather(0, m, slot.up_h.numpy(), lay, self.threads)
+            tick("wait_h2d", t0)
+            t0 = clock()
+            up = slot.up_h.numpy()
+            any_lo, max_pairs, max_track, bad = batch.gather(0, m, up, lay, self.threads)
+            if any_lo:   # values that are not fp32-representable: the low-order stream too
+                batch.gather_lo(0, m, up, lay["uv_lo"], self.threads)
+            else:
+                nbytes = lay["uv_lo"]
+            tick("gather", t0)
+            t0 = clock()
             if bad >= 0:
                 raise IndexError(f"problem {lo + bad}: observation index out of range")
             nc, no, npt = np.diff(co), np.diff(oo), np.diff(po)
@@ -249,7 +300,8 @@ class BatchSolver:
                 st = _lib.stream_ptr()
                 _lib.check(L.mba_pack_obs(m, base + lay["obs_off"], base + lay["pt_off"], base + lay["cam_off"],
                                           base + lay["cam"], base + lay["pt"], base + lay["uv"],
-                                          ptr(slot.rec), ptr(slot.lo) if any_lo else None,
+                                          (base + lay["uv_lo"]) if any_lo else None, ptr(slot.rec),
+                                          ptr(slot.lo) if any_lo else None,
                                           ptr(slot.pack_ws), slot.pack_ws.numel(), st), "mba_pack_obs")
                 c = self._cfg()
                 o = self._outs(slot, lay)
@@ -257,7 +309,13 @@ class BatchSolver:
                 slot.ws = _Slot._grow(slot.ws, need, torch, dtype=torch.uint8, device=self.device)
                 _lib.check(L.mba_solve(ct.byref(d), ct.byref(c), ct.byref(o), ptr(slot.ws), slot.ws.numel(), st),
                            "mba_solve")
-                self.launches += 1 + int(L.mba_solve_launches(ct.byref(d), ct.byref(c)))
+                od = slot.out_d
+                _lib.check(L.mba_compact_traces(m, prm.max_iters, ptr(od["n_iters"]), ptr(od["costs"]),
+                                                ptr(od["lambdas"]), ptr(od["accepted"]), ptr(od["evals"]),
+                                                ptr(od["trace_off"]), ptr(od["c_costs"]), ptr(od["c_lambdas"]),
+                                                ptr(od["c_accepted"]), ptr(od["c_evals"]), st),
+                           "mba_compact_traces")
+                self.launches += 3 + int(L.mba_solve_launches(ct.byref(d), ct.byref(c)))
                 slot.done = torch.cuda.Event()
                 slot.done.record(cs)
             self.back.wait_event(slot.done)
@@ -270,21 +328,38 @@ class BatchSolver:
                 slot.read = torch.cuda.Event()
                 slot.read.record(self.back)
             pending.append((ci, lo, hi, slot, batch, sizes, chunk, norm))
+            tick("enqueue", t0)
+        t0 = clock()
         while pending:
             self._finish(pending.pop(0), res)
+        tick("finish", t0)
         return res
 
     # ------------------------------------------------------------------
     def _out_sizes(self, C, P, m):
-        w = max(self.prm.max_iters, 1)
-        return dict(R=9 * C, t=3 * C, focal=m, points=3 * P, costs=m * (self.prm.max_iters + 1),
-                    lambdas=m * w, accepted=m * w, evals=m * w, n_iters=m, status=m, final_stats=4 * m)
+        return dict(R=9 * C, t=3 * C, focal=m, points=3 * P, n_iters=m, status=m, final_stats=4 * m,
+                    trace_off=m + 1)
 
     def _finish(self, item, res):
+        import time
+        torch = self.torch
         ci, lo, hi, slot, batch, sizes, chunk, norm = item
+        t0 = time.perf_counter()
         slot.read.synchronize()
+        self.host_s["wait_read"] = self.host_s.get("wait_read", 0.0) + time.perf_counter() - t0
         m = hi - lo
         h = {k: slot.out_h[k][:sizes[k]].numpy() for k in _OUT}
+        # the packed traces: only their used prefix crosses PCIe
+        off = h["trace_off"].copy()
+        tot = int(off[-1])
+        with torch.cuda.stream(self.trace_back):
+            for k, n in (("c_costs", tot + m), ("c_lambdas", tot), ("c_accepted", tot), ("c_evals", tot)):
+                slot.out_h[k][:n].copy_(slot.out_d[k][:n], non_blocking=True)
+                self.d2h_bytes += n * slot.out_h[k].element_size()
+        self.trace_back.synchronize()
+        res.add_chunk(lo, hi, off, slot.out_h["c_costs"][:tot + m].numpy().copy(),
+                      slot.out_h["c_lambdas"][:tot].numpy().copy(), slot.out_h["c_accepted"][:tot].numpy().copy(),
+                      slot.out_h["c_evals"][:tot].numpy().copy())
         status = h["status"]
         if np.any(status < 0):
             b = int(np.flatnonzero(status < 0)[0])
@@ -301,11 +376,6 @@ class BatchSolver:
                         p[k] = q[k]
                     else:
                         setattr(p, k, q[k])
-        w = max(self.prm.max_iters, 1)
-        res.costs[lo:hi] = h["costs"].reshape(m, -1)
-        res.lambdas[lo:hi] = h["lambdas"].reshape(m, w)
-        res.accepted[lo:hi] = h["accepted"].reshape(m, w)
-        res.evals[lo:hi] = h["evals"].reshape(m, w)
         res.n_iters[lo:hi] = h["n_iters"]
         res.status[lo:hi] = status
         res.final_stats[lo:hi] = h["final_stats"].reshape(m, 4)

@@ -14,9 +14,10 @@
 //    views that keep every array alive and locked for the batch's lifetime.
 //  * gather(lo, hi, ...): copies problems [lo, hi) into the chunk's upload
 //    buffer (pinned host memory owned by the caller) in the device upload
-//    layout -- int64 indices narrowed to int32, uv kept in float64 (the
-//    device splits it into fp32 + residual), per-point track statistics for
-//    the solver's plan -- on worker threads with the GIL released.
+//    layout -- int64 indices narrowed to int32, uv rounded to float32 with a
+//    note whether any value is not fp32-representable (gather_lo then writes
+//    the low-order float32 residual stream for that chunk), per-point track
+//    statistics for the solver's plan -- on worker threads, GIL released.
 //  * scatter(lo, hi, ...): writes the solved R, t, points back into the
 //    callers' arrays in place (threads, GIL released) and rebinds focal.
 //
@@ -289,17 +290,27 @@ void narrow(const I* __restrict__ src, int32_t* __restrict__ dst, int64_t K, int
   hi = (int64_t)mx;
 }
 
-int needs_lo(const double* __restrict__ x, int64_t n) {
+// float32 rounding; returns whether any value is not fp32-representable
+int to_f32(const double* __restrict__ x, float* __restrict__ y, int64_t n) {
   int r = 0;
-  for (int64_t k = 0; k < n; ++k) r |= (double)(float)x[k] != x[k];
+  for (int64_t k = 0; k < n; ++k) {
+    const float v = (float)x[k];
+    y[k] = v;
+    r |= (double)v != x[k];
+  }
   return r;
+}
+
+// low-order stream: (float)(x - (double)(float)x)
+void lo_f32(const double* __restrict__ x, float* __restrict__ y, int64_t n) {
+  for (int64_t k = 0; k < n; ++k) y[k] = (float)(x[k] - (double)(float)x[k]);
 }
 
 // gather(lo, hi, buf, layout, threads) -> (any_lo, max_pairs, max_track, bad)
 // layout: byte offsets of the regions inside `buf` (a dict from the Python
 // side): cam_off, pt_off, obs_off (int64, m+1, chunk-relative), fixed (u8),
 // cx, cy, focal (f64, m), flags (u8, m), R (f64 9n), t (f64 3n), points
-// (f64 3P), cam, pt (i32 K), uv (f64 2K).
+// (f64 3P), cam, pt (i32 K), uv (f32 2K: uv rounded to float).
 PyObject* batch_gather(BatchObj* self, PyObject* args) {
   Py_ssize_t lo, hi;
   PyObject *bufo, *lay;
@@ -333,7 +344,7 @@ PyObject* batch_gather(BatchObj* self, PyObject* args) {
   // bounds of the destination regions
   const int64_t need[14] = {8 * (m + 1), 8 * (m + 1), 8 * (m + 1), co[hi] - c0, 8 * m, 8 * m, 8 * m, m,
                             72 * (co[hi] - c0), 24 * (co[hi] - c0), 24 * (po[hi] - p0), 4 * (oo[hi] - k0),
-                            4 * (oo[hi] - k0), 16 * (oo[hi] - k0)};
+                            4 * (oo[hi] - k0), 8 * (oo[hi] - k0)};
   for (int k = 0; k < 14; ++k)
     if (off[k] < 0 || off[k] + need[k] > buf.len) {
       PyErr_Format(PyExc_ValueError, "layout region '%s' outside the buffer", names[k]);
@@ -388,10 +399,9 @@ PyObject* batch_gather(BatchObj* self, PyObject* args) {
         continue;
       }
       for (int64_t k = 0; k < q.K; ++k) ++cnt[(size_t)dp[k]];
-      // uv in float64 (the device splits it); note whether any value needs the
-      // low-order fp32 correction stream
-      memcpy(base + off[13] + 16 * kk, q.uv, 16 * q.K);
-      if (!any_lo[r]) any_lo[r] = needs_lo(q.uv, 2 * q.K);
+      // uv rounded to float32; note whether any value needs the low-order
+      // correction stream (gather_lo)
+      any_lo[r] |= to_f32(q.uv, (float*)(base + off[13]) + 2 * kk, 2 * q.K);
       int64_t pairs = 0, mt = 0;
       for (int64_t p = 0; p < q.P; ++p) {
         const int64_t v = cnt[(size_t)p];
@@ -413,6 +423,39 @@ PyObject* batch_gather(BatchObj* self, PyObject* args) {
     mt = std::max(mt, max_track[r]);
   }
   return Py_BuildValue("(OLLi)", a ? Py_True : Py_False, (long long)mp, (long long)mt, b);
+}
+
+// gather_lo(lo, hi, buf, offset, threads): the low-order float32 uv stream of
+// problems [lo, hi) at byte `offset` of `buf` (only for chunks whose gather
+// reported a value that is not fp32-representable)
+PyObject* batch_gather_lo(BatchObj* self, PyObject* args) {
+  Py_ssize_t lo, hi;
+  PyObject* bufo;
+  long long off;
+  int nt = 1;
+  if (!PyArg_ParseTuple(args, "nnOL|i", &lo, &hi, &bufo, &off, &nt)) return nullptr;
+  const Py_ssize_t B = (Py_ssize_t)self->probs->size();
+  if (lo < 0 || hi > B || lo > hi) {
+    PyErr_SetString(PyExc_IndexError, "problem range out of bounds");
+    return nullptr;
+  }
+  const auto& oo = *self->obs_off;
+  const int64_t k0 = oo[lo];
+  Py_buffer buf;
+  if (!writable_view(bufo, &buf, "gather_lo", off + 8 * (oo[hi] - k0))) return nullptr;
+  if (nt < 1) nt = 1;
+  if (nt > 64) nt = 64;
+  if ((int64_t)nt > hi - lo) nt = (int)std::max<Py_ssize_t>(hi - lo, 1);
+  const auto cut = split(oo, lo, hi, nt);
+  float* dst = (float*)((char*)buf.buf + off);
+  const std::vector<Prob>& probs = *self->probs;
+  Py_BEGIN_ALLOW_THREADS
+  run_threads(nt, [&](int r) {
+    for (Py_ssize_t i = cut[r]; i < cut[r + 1]; ++i) lo_f32(probs[i].uv, dst + 2 * (oo[i] - k0), 2 * probs[i].K);
+  });
+  Py_END_ALLOW_THREADS
+  PyBuffer_Release(&buf);
+  Py_RETURN_NONE;
 }
 
 // scatter(lo, hi, R, t, focal, points, threads) -> list of problem indices
@@ -492,6 +535,8 @@ PyObject* batch_offsets(BatchObj* self, PyObject*) {
 PyMethodDef batch_methods[] = {
     {"gather", (PyCFunction)batch_gather, METH_VARARGS,
      "gather(lo, hi, buf, layout, threads=1) -> (any_lo, max_pairs, max_track, first_bad)"},
+    {"gather_lo", (PyCFunction)batch_gather_lo, METH_VARARGS,
+     "gather_lo(lo, hi, buf, byte_offset, threads=1): low-order float32 uv stream"},
     {"scatter", (PyCFunction)batch_scatter, METH_VARARGS,
      "scatter(lo, hi, R, t, focal, points, threads=1) -> problems to rebind"},
     {"offsets", (PyCFunction)batch_offsets, METH_NOARGS, "(cam_off, pt_off, obs_off) int64 bytes"},

@@ -20,7 +20,8 @@ def main():
     ap.add_argument("--problems", type=int, default=65536)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--precision", default="f64")
-    ap.add_argument("--chunks", type=int, default=8)
+    ap.add_argument("--chunks", type=int, default=16)
+    ap.add_argument("--ring", type=int, default=4)
     ap.add_argument("--threads", type=int, default=0)
     a = ap.parse_args()
     import torch
@@ -38,7 +39,7 @@ def main():
         probs.append(BaProblem(**p))
     init = [(p.R.copy(), p.t.copy(), p.focal, p.points.copy()) for p in probs]
     gen = time.perf_counter() - t0
-    bs = BatchSolver(None, n_chunks=a.chunks, threads=a.threads or None)
+    bs = BatchSolver(None, n_chunks=a.chunks, threads=a.threads or None, ring=a.ring)
     _SOLVERS[torch.cuda.current_device()] = bs
     cfg = LmConfig(max_iters=200)
     times = []
@@ -61,6 +62,7 @@ def main():
                       "problems_per_s": a.problems / float(np.median(times)),
                       "h2d_bytes": bs.h2d_bytes, "d2h_bytes": bs.d2h_bytes,
                       "mean_iters": float(np.mean(infos.n_iters)), "status_ok": int(np.sum(st >= 0)),
+                      "host_s_last_call": bs.host_s,
                       "gen_s": gen}))
 
 

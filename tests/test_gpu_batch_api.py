@@ -25,12 +25,14 @@ def _pack_device(problems, with_lo):
     cam = np.concatenate([p["cam_idx"] for p in problems]).astype(np.int32)
     pt = np.concatenate([p["pt_idx"] for p in problems]).astype(np.int32)
     uv = np.concatenate([p["uv"] for p in problems]).astype(np.float64)
+    uv32 = uv.astype(np.float32)
+    uvlo = (uv - uv32.astype(np.float64)).astype(np.float32)   # the host gather's streams
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     K = int(oo[-1])
     rec = torch.zeros((K, 4), dtype=torch.float32, device="cuda")
     lo = torch.zeros((K, 2), dtype=torch.float32, device="cuda") if with_lo else None
     ws = torch.empty(int(L.mba_pack_obs_workspace_bytes(int(po[-1]))), dtype=torch.uint8, device="cuda")
-    args = [d(oo), d(po), d(co), d(cam), d(pt), d(uv)]
+    args = [d(oo), d(po), d(co), d(cam), d(pt), d(uv32), d(uvlo) if with_lo else None]
     rc = L.mba_pack_obs(len(problems), *[ptr(a) for a in args], ptr(rec), ptr(lo), ptr(ws), ws.numel(),
                         _lib.stream_ptr())
     assert rc == 0

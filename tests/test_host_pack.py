@@ -45,8 +45,8 @@ def test_gather_matches_numpy_concatenation():
     assert len(hb) == len(probs) and bad == -1 and not any_lo
     K, P, C = int(oo[-1]), int(po[-1]), int(co[-1])
     np.testing.assert_array_equal(region(buf, lay, "obs_off", np.int64, len(probs) + 1), oo)
-    np.testing.assert_array_equal(region(buf, lay, "uv", np.float64, 2 * K),
-                                  np.concatenate([p.uv for p in probs]).ravel())
+    np.testing.assert_array_equal(region(buf, lay, "uv", np.float32, 2 * K),
+                                  np.concatenate([p.uv for p in probs]).ravel().astype(np.float32))
     np.testing.assert_array_equal(region(buf, lay, "cam", np.int32, K),
                                   np.concatenate([p.cam_idx for p in probs]))
     np.testing.assert_array_equal(region(buf, lay, "pt", np.int32, K),
@@ -69,6 +69,15 @@ def test_gather_is_thread_count_invariant_and_flags_low_order_uv():
     for o in outs[1:]:
         np.testing.assert_array_equal(o[3], outs[0][3])
     assert all(o[4][0] for o in outs)
+    # the low-order stream reconstructs the exact float64 pixels
+    hb, (co, po, oo), lay, buf, _ = outs[0]
+    hb.gather_lo(0, len(probs), buf, lay["uv_lo"], 3)
+    K = int(oo[-1])
+    hi32 = region(buf, lay, "uv", np.float32, 2 * K).astype(np.float64)
+    lo32 = region(buf, lay, "uv_lo", np.float32, 2 * K).astype(np.float64)
+    uv = np.concatenate([p.uv for p in probs]).ravel()
+    np.testing.assert_array_equal(lo32, (uv - hi32).astype(np.float32).astype(np.float64))
+    assert np.abs(hi32 + lo32 - uv).max() < 1e-12
 
 
 def test_scatter_writes_in_place_and_rebinds_focal():
