@@ -74,7 +74,46 @@ def main():
         err = max(np.abs(p.R - R).max() for p, R in zip(poses, z["out_R"]))
         out.append({"seed": seed, "median_s": float(np.median(ts)), "focal": float(intr_out.focal),
                     "ref_focal": float(z["out_focal"]), "max_R_diff_vs_reference_output": float(err)})
-    print(json.dumps({"metric": "bootstrap wall time (SURVEY 8(f)-2)",
+    batched = None
+    if not a.ref:
+        # many windows through ONE device schedule (bootstrap_batch): the 20
+        # acceptance windows (tests/golden/bootstrap20.npz) replicated
+        z20 = np.load(f"{GOLDEN}/bootstrap20.npz")
+        wins, o = [], 0
+        counts = z20["counts"].reshape(20, -1)
+        for s_ in range(20):
+            w = []
+            for c in counts[s_]:
+                w.append((z20["kp"][o:o + c], z20["ids"][o:o + c]))
+                o += c
+            wins.append(w)
+        intrs = [CameraIntrinsics(float(z20["focal"][s_]), float(z20["cx"][s_]), float(z20["cy"][s_]),
+                                  int(z20["width"][s_]), int(z20["height"][s_])) for s_ in range(20)]
+        reps = 8
+        W, I = wins * reps, intrs * reps
+        M.bootstrap_batch(W, I, CaptureConfig(), matcher=_matcher)
+        sync()
+        from gsrecon import _bootstrap as B_
+        sched_s = []
+        orig = B_.schedule_batch
+
+        def timed(*args, **kw):
+            t = time.perf_counter()
+            out = orig(*args, **kw)
+            sched_s.append(time.perf_counter() - t)
+            return out
+        B_.schedule_batch = timed
+        t0 = time.perf_counter()
+        res = M.bootstrap_batch(W, I, CaptureConfig(), matcher=_matcher)
+        sync()
+        dt = time.perf_counter() - t0
+        B_.schedule_batch = orig
+        batched = {"windows": len(W), "seconds": dt, "bootstraps_per_s": len(W) / dt,
+                   "device_schedule_seconds": sched_s,
+                   "schedule_bootstraps_per_s": len(W) / sched_s[0] if sched_s else None,
+                   "failures": sum(isinstance(r, Exception) for r in res),
+                   "note": "host track building (exact matcher) + one device schedule + the rescue schedule"}
+    print(json.dumps({"metric": "bootstrap wall time (SURVEY 8(f)-2)", "batched": batched,
                       "impl": "reference (CPU, numpy/scipy)" if a.ref else "this package (device lm_solve)",
                       "cores": len(os.sched_getaffinity(0)), "runs": out}))
 
