@@ -194,9 +194,9 @@ def test_cluster_kernel_plans(cuda_ok):
     assert solver.plan(big, solver.LmParams(precision="f64")) == 16
     assert solver.plan(big, solver.LmParams(precision="mixed")) == 8
     # a full batch of config-3 problems: the planner scores the fitting cluster
-    # sizes by resident clusters (B200: 10 in f64, 9 in mixed)
+    # sizes by resident clusters (B200: 9 in both precisions)
     full = solver.to_device(solver.pack_synth(make_batch(64, n_cams=8, K=20000, seed=3)))
-    assert solver.plan(full, solver.LmParams(precision="f64")) in (10, 12, 16)
+    assert solver.plan(full, solver.LmParams(precision="f64")) in (9, 10, 12, 16)
     assert solver.plan(full, solver.LmParams(precision="mixed")) in (8, 9, 10, 12, 16)
 
 
@@ -317,7 +317,7 @@ def _oracle_job(args):
 def test_config3_full_batch_on_production_plan(precision, cuda_ok):
     """BASELINE config 3 shape at its stated size: a full batch of 64 problems
     of 8 frames x K = 20k goes through the auto planner's production plan
-    (B200: 10-CTA clusters in f64, 9 in mixed, scored by resident clusters),
+    (B200: 9-CTA clusters in both precisions, scored by resident clusters),
     and problems spread over the batch match the CPU oracle under the parity
     rule."""
     from concurrent.futures import ProcessPoolExecutor
@@ -326,7 +326,7 @@ def test_config3_full_batch_on_production_plan(precision, cuda_ok):
     b = make_batch(64, n_cams=8, K=20000, seed=0)
     probs = [b.problem(i) for i in range(64)]
     plan = solver.plan(solver.to_device(solver.pack_problems(probs)), solver.LmParams(precision=precision))
-    assert plan == (10 if precision == "f64" else 9), plan
+    assert plan == 9, plan
     dev = run_device(probs, dict(max_iters=200), precision, "auto")
     pick = (0, 21, 42, 63)
     with ProcessPoolExecutor(4) as ex:
