@@ -156,14 +156,18 @@ __global__ void __launch_bounds__(kThreads) filter_kernel(FilterArgs A) {
     A.keep[ob + k] = kk;
     kept += kk;
   }
-  kept = __syncthreads_count(kept) > 0 ? kept : kept;   // (barrier before the alive flags)
-  __shared__ int s_kept;
-  if (threadIdx.x == 0) s_kept = 0;
-  __syncthreads();
-  atomicAdd(&s_kept, kept);
   for (int p = threadIdx.x; p < P; p += blockDim.x) A.pt_alive[pb + p] = A.count[pb + p] >= 2;
+  // block total of the survivors (fixed order: warp sums, then warps in order)
+  __shared__ int s_wk[kThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
+  if ((threadIdx.x & 31) == 0) s_wk[threadIdx.x >> 5] = kept;
   __syncthreads();
-  if (threadIdx.x == 0) A.n_kept[b] = s_kept;
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < kThreads / 32; ++w) tot += s_wk[w];
+    A.n_kept[b] = tot;
+  }
 }
 
 // obs_off2 = exclusive scan of n_kept (one block)

@@ -73,13 +73,29 @@ __global__ void __launch_bounds__(kTile * 4) tile_kernel(const uint32_t* __restr
     sb[r][w] = rb < nb ? __ldg(desc + (b0 + rb) * kWords + w) : 0u;
   }
   __syncthreads();
-  // the tile's distances, each computed once
-  for (int i = tid; i < kTile * kTile; i += blockDim.x) {
-    const int r = i / kTile, c = i % kTile;
-    int d = 0;
+  // the tile's distances, each computed once: a 4 x 4 register block per
+  // thread (4 rows of A and 4 columns of B held in registers, 4 shared loads
+  // per distance instead of 16)
+  for (int blk = tid; blk < (kTile / 4) * (kTile / 4); blk += blockDim.x) {
+    const int r0 = (blk / (kTile / 4)) * 4, c0 = (blk % (kTile / 4)) * 4;
+    int d[4][4] = {};
 #pragma unroll
-    for (int w = 0; w < kWords; ++w) d += __popc(sa[r][w] ^ sb[c][w]);
-    dist[r][c] = (unsigned short)d;
+    for (int w = 0; w < kWords; ++w) {
+      uint32_t a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = sa[r0 + q][w];
+        b[q] = sb[c0 + q][w];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[i][j] += __popc(a[i] ^ b[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dist[r0 + i][c0 + j] = (unsigned short)d[i][j];
   }
   __syncthreads();
   const int64_t ra_left = na - (int64_t)ta * kTile, rb_left = nb - (int64_t)tb * kTile;

@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(int n_problems, const in
                                                         const float2* __restrict__ uv_lo, MbaObs* __restrict__ out,
                                                         float2* __restrict__ out_lo, int32_t* __restrict__ gcount) {
   __shared__ int s_cnt[kSmemCounts];
-  __shared__ int s_bad, s_unsorted, s_wsum[kThreads / 32];
+  __shared__ int s_wsum[kThreads / 32];
   const int b = blockIdx.x;
   if (b >= n_problems) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -60,11 +60,6 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(int n_problems, const in
   const int K = (int)(obs_off[b + 1] - k0);
   const int P = (int)(pt_off[b + 1] - pt_off[b]);
   const int n = (int)(cam_off[b + 1] - cam_off[b]);
-  if (tid == 0) {
-    s_bad = 0;
-    s_unsorted = 0;
-  }
-  __syncthreads();
   int bad = 0, uns = 0;
   for (int k = tid; k < K; k += kThreads) {
     const int c = __ldg(cam + k0 + k), p = __ldg(pt + k0 + k);

@@ -341,6 +341,8 @@ def bootstrap_batch(windows: list, intrs: list, cfg: CaptureConfig, matcher=None
     metas, probs = [], []
     for features, intr in zip(windows, intrs):
         n = len(features)
+        if n > 64:   # the device gauge step holds up to 64 camera centres per window
+            raise ValueError(f"bootstrap window of {n} frames (at most 64)")
         tracks = build_tracks_device(features) if matcher is None else build_tracks(features, matcher)
         if len(tracks) < M.MIN_BOOTSTRAP_TRACKS:
             metas.append(M.BootstrapFailure(f"{len(tracks)} tracks < {M.MIN_BOOTSTRAP_TRACKS}"))
