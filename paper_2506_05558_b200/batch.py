@@ -83,13 +83,16 @@ class BatchResult:
         self.n_iters = np.zeros(B, np.int32)
         self.status = np.zeros(B, np.int32)
         self.final_stats = np.zeros((B, 4))
-        self._starts = []       # first problem of each stored chunk
-        self._chunks = []       # (lo, hi, off, costs, lambdas, accepted, evals)
+        self._where = np.full(B, -1, np.int32)   # stored chunk of each problem
+        self._pos = np.zeros(B, np.int32)        # its row inside that chunk
+        self._chunks = []       # (off, costs, lambdas, accepted, evals)
         self._override = {}
 
-    def add_chunk(self, lo, hi, off, costs, lambdas, accepted, evals):
-        self._starts.append(lo)
-        self._chunks.append((lo, hi, off, costs, lambdas, accepted, evals))
+    def add_chunk(self, index, off, costs, lambdas, accepted, evals):
+        """Packed traces of the problems `index` (global indices, chunk order)."""
+        self._where[index] = len(self._chunks)
+        self._pos[index] = np.arange(len(index), dtype=np.int32)
+        self._chunks.append((off, costs, lambdas, accepted, evals))
 
     def __len__(self):
         return len(self.n_iters)
@@ -103,9 +106,8 @@ class BatchResult:
             raise IndexError(b)
         if b in self._override:
             return dict(self._override[b])
-        import bisect
-        lo, hi, off, c, lam, acc, ev = self._chunks[bisect.bisect_right(self._starts, b) - 1]
-        j = b - lo
+        off, c, lam, acc, ev = self._chunks[self._where[b]]
+        j = int(self._pos[b])
         o0, o1 = int(off[j]), int(off[j + 1])
         st = self.final_stats[b]
         K = max(st[3], 1.0)
@@ -187,7 +189,8 @@ class BatchSolver:
     points written in place when the arrays are writable float64, rebound
     otherwise; focal rebound) and returns a `BatchResult`."""
 
-    def __init__(self, prm, n_chunks=16, min_chunk=512, threads=None, device=None, ring=4):
+    def __init__(self, prm, n_chunks=16, min_chunk=512, threads=None, device=None, ring=4,
+                 oversize=None, max_cams=32):
         torch = _lib.torch_cuda()
         self.torch = torch
         self.prm = prm
@@ -203,6 +206,10 @@ class BatchSolver:
         self.slots = [_Slot(torch, self.device) for _ in range(ring)]
         self.h2d_bytes = self.d2h_bytes = 0
         self.launches = 0
+        # problems with more cameras than mba_solve's fused kernels hold go to
+        # `oversize(problem) -> info dict` (the stage-kernel loop)
+        self.oversize = oversize
+        self.max_cams = max_cams
 
     def chunks(self, B):
         """Chunk boundaries. With enough chunks the first and last two are
@@ -259,8 +266,24 @@ class BatchSolver:
                 # views): solve normalised copies, then rebind the results
                 norm = [normalise(p) for p in chunk]
                 batch = H.Batch(norm)
-            m = hi - lo
             co, po, oo = (np.frombuffer(x, np.int64) for x in batch.offsets())
+            index = np.arange(lo, hi)
+            over = np.flatnonzero(np.diff(co) > self.max_cams)
+            if len(over):   # rare: solve those problems outside the batch, keep the rest
+                if self.oversize is None:
+                    raise ValueError(f"problem {lo + int(over[0])} has more than {self.max_cams} cameras")
+                for j in over:
+                    res.set(lo + int(j), self.oversize(chunk[j]))
+                keep = np.setdiff1d(np.arange(hi - lo), over)
+                if not len(keep):
+                    continue
+                index = lo + keep
+                chunk = [chunk[j] for j in keep]
+                if norm is not None:
+                    norm = [norm[j] for j in keep]
+                batch = H.Batch(norm if norm is not None else chunk)
+                co, po, oo = (np.frombuffer(x, np.int64) for x in batch.offsets())
+            m = len(index)
             C, P, K = int(co[-1]), int(po[-1]), int(oo[-1])
             lay, nbytes = layout(C, P, K, m)
             slot.ensure(nbytes, K, P, C, m, prm.max_iters)
@@ -279,7 +302,7 @@ class BatchSolver:
             tick("gather", t0)
             t0 = clock()
             if bad >= 0:
-                raise IndexError(f"problem {lo + bad}: observation index out of range")
+                raise IndexError(f"problem {int(index[bad])}: observation index out of range")
             nc, no, npt = np.diff(co), np.diff(oo), np.diff(po)
             d = self._desc(slot, lay, m, int(nc.max()), int(no.max()), int(npt.max()), max_pairs,
                            max_track, any_lo)
@@ -327,7 +350,7 @@ class BatchSolver:
                     self.d2h_bytes += n * slot.out_h[k].element_size()
                 slot.read = torch.cuda.Event()
                 slot.read.record(self.back)
-            pending.append((ci, lo, hi, slot, batch, sizes, chunk, norm))
+            pending.append((ci, index, slot, batch, sizes, chunk, norm))
             tick("enqueue", t0)
         t0 = clock()
         while pending:
@@ -343,11 +366,12 @@ class BatchSolver:
     def _finish(self, item, res):
         import time
         torch = self.torch
-        ci, lo, hi, slot, batch, sizes, chunk, norm = item
+        ci, index, slot, batch, sizes, chunk, norm = item
+        lo = int(index[0])
         t0 = time.perf_counter()
         slot.read.synchronize()
         self.host_s["wait_read"] = self.host_s.get("wait_read", 0.0) + time.perf_counter() - t0
-        m = hi - lo
+        m = len(index)
         h = {k: slot.out_h[k][:sizes[k]].numpy() for k in _OUT}
         # the packed traces: only their used prefix crosses PCIe
         off = h["trace_off"].copy()
@@ -357,13 +381,13 @@ class BatchSolver:
                 slot.out_h[k][:n].copy_(slot.out_d[k][:n], non_blocking=True)
                 self.d2h_bytes += n * slot.out_h[k].element_size()
         self.trace_back.synchronize()
-        res.add_chunk(lo, hi, off, slot.out_h["c_costs"][:tot + m].numpy().copy(),
+        res.add_chunk(index, off, slot.out_h["c_costs"][:tot + m].numpy().copy(),
                       slot.out_h["c_lambdas"][:tot].numpy().copy(), slot.out_h["c_accepted"][:tot].numpy().copy(),
                       slot.out_h["c_evals"][:tot].numpy().copy())
         status = h["status"]
         if np.any(status < 0):
             b = int(np.flatnonzero(status < 0)[0])
-            raise ValueError(f"problem {lo + b}: malformed problem (status {int(status[b])})")
+            raise ValueError(f"problem {int(index[b])}: malformed problem (status {int(status[b])})")
         rebind = batch.scatter(0, m, h["R"], h["t"], h["focal"], h["points"], self.threads)
         if rebind:
             self._rebind(batch, norm if norm is not None else chunk, rebind, h)
@@ -376,9 +400,9 @@ class BatchSolver:
                         p[k] = q[k]
                     else:
                         setattr(p, k, q[k])
-        res.n_iters[lo:hi] = h["n_iters"]
-        res.status[lo:hi] = status
-        res.final_stats[lo:hi] = h["final_stats"].reshape(m, 4)
+        res.n_iters[index] = h["n_iters"]
+        res.status[index] = status
+        res.final_stats[index] = h["final_stats"].reshape(m, 4)
 
     def _rebind(self, batch, chunk, idx, h):
         """Problems whose arrays are read-only get new arrays (the reference

@@ -261,25 +261,15 @@ def lm_solve_batch(problems, cfg: LmConfig, precision: str | None = None):
     prm = solver.LmParams.from_cfg(cfg)
     if precision is not None:
         prm.precision = precision
-    problems = list(problems)
-    big = [i for i, p in enumerate(problems) if len(np.asarray(p.R).reshape(-1, 9)) > MAX_FUSED_CAMS]
-    if big:
-        # more cameras than the fused kernel holds: the stage-kernel loop
-        from paper_2506_05558_b200.batch import BatchResult
-        small = [i for i in range(len(problems)) if i not in set(big)]
-        part = lm_solve_batch([problems[i] for i in small], cfg, precision) if small else None
-        res = BatchResult(len(problems), prm.max_iters)
-        for j, i in enumerate(small):
-            res.set(i, part[j])
-        for i in big:
-            res.set(i, _lm_stages(problems[i], cfg, "schur"))
-        return res
     torch = _torch()
     key = torch.cuda.current_device()
     bs = _SOLVERS.get(key)
     if bs is None:
         bs = _SOLVERS[key] = BatchSolver(prm)
     bs.prm = prm
+    # more cameras than the fused kernel holds: the stage-kernel loop
+    bs.oversize = lambda p: _lm_stages(p, cfg, "schur")
+    bs.max_cams = MAX_FUSED_CAMS
     res = bs.solve(problems)
     torch.cuda.current_stream().wait_stream(bs.back)
     return res
