@@ -95,6 +95,9 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size
 // LDL^T elimination performs the forward substitution on the fly. acol(j) is
 // the start of column j; tab[] maps a packed position to its (row, column).
 __host__ __device__ __forceinline__ int acol(int j, int C) { return j * (C + 1) - (j * (j - 1)) / 2; }
+}  // namespace mba
+#include "mba_ldl.cuh"
+namespace mba {
 
 template <typename T, int MAXC>
 struct Layout {
@@ -109,8 +112,8 @@ struct Layout {
   static constexpr size_t oS = oRed + 8 * kWarps * 4;               // T[CA]
   static constexpr size_t oRhs = align16(oS + sizeof(T) * CA);      // T[C] LDL^T pivot reciprocals
   static constexpr size_t oL10 = align16(oRhs + sizeof(T) * C);     // T[C] LDL^T pair multipliers
-  static constexpr size_t oTab = align16(oL10 + sizeof(T) * C);     // uint16[CA] (row << 8 | col)
-  static constexpr size_t oUcam = align16(oTab + 2 * CA);           // T[N][kUcamStride]
+  static constexpr size_t oTab = align16(oL10 + sizeof(T) * C);     // T[kLdlPanel][ldl_lstr(C)] LDL^T panel L
+  static constexpr size_t oUcam = align16(oTab + sizeof(T) * kLdlPanel * ldl_lstr(C));  // T[N][kUcamStride]
   static constexpr size_t oCamPtr = align16(oUcam + sizeof(T) * N * kUcamStride);
   static constexpr size_t oSlot = oCamPtr + 4 * (N + 1);
   static constexpr size_t oCos = oSlot + 4 * N;
@@ -374,7 +377,6 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   struct {
     double *Rc, *tc, *Rt, *tt, *dc, *red;
     T *S, *rhs, *ucam;
-    unsigned short* tab;
     int *cam_ptr, *slot, *cam_of_slot, *blk_off;
     unsigned char *blk_a, *blk_b;
   } sm;
@@ -387,7 +389,6 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   sm.S = (T*)(smem_raw + L::oS);
   sm.rhs = (T*)(smem_raw + L::oRhs);
   sm.ucam = (T*)(smem_raw + L::oUcam);
-  sm.tab = (unsigned short*)(smem_raw + L::oTab);
   sm.cam_ptr = (int*)(smem_raw + L::oCamPtr);
   sm.slot = (int*)(smem_raw + L::oSlot);
   sm.cam_of_slot = (int*)(smem_raw + L::oCos);
@@ -592,11 +593,6 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       for (int q = 0; q < nb; ++q) sm.blk_off[q + 1] = sm.blk_off[q] + blk_cnt[q + 1];
     }
     __syncthreads();
-  }
-  // packed position -> (row, col) table of the augmented system
-  for (int j = tid; j < C; j += blockDim.x) {
-    const int a0 = acol(j, C);
-    for (int i = j; i <= C; ++i) sm.tab[a0 + i - j] = (unsigned short)((i << 8) | j);
   }
   const int CA = C * (C + 3) / 2;
   // cooperative mode: the job chunk table (job, first item) and chunks per job
@@ -943,105 +939,12 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     __syncthreads();
     PROF_MARK(PH_ASM)
 
-    // ---------- K4 LDL^T of the augmented system, two pivots per barrier ----------
-    // Right-looking rank-2 steps (as in mba_v4.cu): pivots k and k+1 are formed
-    // redundantly by every thread, the trailing entries (columns >= k+2, a
-    // contiguous packed range; tab gives row / column) receive both updates at
-    // once with column k+1 corrected on the fly, and column k+1 is finalised
-    // lazily during the next step. The rhs row ends up holding the forward-
-    // substituted y; S[k][k] keeps d_k, S[i][k] keeps L_ik d_k, invd[k] = 1/d_k.
-    bool chol_fail = false;
+    // ---------- K4 LDL^T of the augmented system (mba_ldl.cuh) ----------
+    bool chol_fail;
     {
-      T* invd = sm.rhs;
-      T* l10s = (T*)(smem_raw + L::oL10);
-      auto bad_pivot = [](T d) { return !(d > T(0)) || !isfinite((double)d); };
-      int k = 0, pend = -1;
-      for (; k + 1 < C; k += 2) {
-        const T* colk = sm.S + acol(k, C) - k;
-        const T* colk1 = sm.S + acol(k + 1, C) - (k + 1);
-        const T d0 = colk[k], a10 = colk[k + 1], d1r = colk1[k + 1];
-        if (bad_pivot(d0)) {
-          chol_fail = true;
-          break;
-        }
-        const T i0 = T(1) / d0;
-        const T l10 = a10 * i0;
-        const T d1 = d1r - l10 * a10;
-        if (bad_pivot(d1)) {
-          chol_fail = true;
-          break;
-        }
-        const T i1 = T(1) / d1;
-        if (tid == 0) {
-          invd[k] = i0;
-          invd[k + 1] = i1;
-          l10s[k] = l10;
-        }
-        // four entries per thread in flight (the loads form short dependent
-        // chains: tab -> column entries -> update)
-        const int e0 = acol(k + 2, C) + tid;
-        const int NTB = blockDim.x;
-        int e = e0;
-        for (; e + 3 * NTB < CA; e += 4 * NTB) {
-          unsigned ij[4];
-          T ai[4], aj[4], ci[4], cj[4], sv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) ij[u] = sm.tab[e + u * NTB];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int ii = (int)(ij[u] >> 8), jj = (int)(ij[u] & 255u);
-            ai[u] = colk[ii];
-            aj[u] = colk[jj];
-            ci[u] = colk1[ii];
-            cj[u] = colk1[jj];
-            sv[u] = sm.S[e + u * NTB];
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const T ci1 = ci[u] - ai[u] * l10, cj1 = cj[u] - aj[u] * l10;
-            sm.S[e + u * NTB] = sv[u] - ai[u] * aj[u] * i0 - ci1 * cj1 * i1;
-          }
-        }
-        for (; e < CA; e += NTB) {
-          const unsigned ij = sm.tab[e];
-          const int ii = (int)(ij >> 8), jj = (int)(ij & 255u);
-          const T ai = colk[ii], aj = colk[jj], ci = colk1[ii], cj = colk1[jj];
-          const T ci1 = ci - ai * l10, cj1 = cj - aj * l10;
-          sm.S[e] = sm.S[e] - ai * aj * i0 - ci1 * cj1 * i1;
-        }
-        if (pend >= 0) {   // finalise column pend (= k - 1) against column pend - 1
-          T* cp = sm.S + acol(pend, C) - pend;
-          const T* cq = sm.S + acol(pend - 1, C) - (pend - 1);
-          const T lp = l10s[pend - 1];
-          for (int i = pend + tid; i <= C; i += blockDim.x) cp[i] = cp[i] - cq[i] * lp;
-        }
-        pend = k + 1;
-        __syncthreads();
-      }
-      if (!chol_fail) {
-        if (pend >= 0) {
-          T* cp = sm.S + acol(pend, C) - pend;
-          const T* cq = sm.S + acol(pend - 1, C) - (pend - 1);
-          const T lp = l10s[pend - 1];
-          for (int i = pend + tid; i <= C; i += blockDim.x) cp[i] = cp[i] - cq[i] * lp;
-          __syncthreads();
-        }
-        if (k < C) {   // odd C: the last pivot alone
-          const T* colk = sm.S + acol(k, C) - k;
-          const T d = colk[k];
-          if (bad_pivot(d)) {
-            chol_fail = true;
-          } else {
-            const T inv = T(1) / d;
-            for (int e = acol(k + 1, C) + tid; e < CA; e += blockDim.x) {
-              const unsigned ij = sm.tab[e];
-              sm.S[e] -= colk[ij >> 8] * colk[ij & 255u] * inv;
-            }
-            if (tid == 0) invd[k] = inv;
-          }
-          __syncthreads();
-        }
-      }
+      __shared__ T s_ltop[kLdlPanel * kLdlPanel];
+      __shared__ int s_bad;
+      chol_fail = ldl_blocked<T, NT>(sm.S, C, sm.rhs, (T*)(smem_raw + L::oTab), s_ltop, &s_bad);
     }
     if (it < 64 && ((cfg.fail_iters_mask >> it) & 1ull)) chol_fail = true;
     PROF_MARK(PH_CHOL)
