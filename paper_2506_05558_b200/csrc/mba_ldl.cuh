@@ -198,4 +198,51 @@ __device__ bool ldl_blocked(T* S, int C, T* invd, T* lst, T* s_ltop, int* s_bad)
   return false;
 }
 
+// Back substitution D L^T x = y on the factorised system, blocked like the
+// factorisation (panels of 8 from the bottom): warp 0 solves the panel's 8 x 8
+// unit triangle (x_p = u_p / d_p, u_q -= L_pq d_q x_p), then every thread
+// j < k folds the panel's x into its u_j with 8 contiguous loads from column j
+// (u_j -= sum_p S(k+p, j) x_{k+p}). `u` is scratch for C values of T; the
+// result goes to x_out (double). Two barriers per 8 columns; the column-
+// oriented single-warp scheme it replaces spent ~730 cycles per column.
+template <typename T, int NT>
+__device__ void ldl_backsub(const T* S, int C, const T* invd, T* u, double* x_out) {
+  constexpr int PW = kLdlPanel;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int j = tid; j < C; j += NT) u[j] = S[acol(j, C) + C - j];
+  __syncthreads();
+  for (int k = ((C - 1) / PW) * PW; k >= 0; k -= PW) {
+    const int w = C - k < PW ? C - k : PW;
+    if (wid == 0) {
+      T up = lane < w ? u[k + lane] : T(0);
+      const T il = lane < w ? invd[k + lane] : T(0);
+      const int bl = acol(k + lane, C) - (k + lane) + k;   // S(k + p, k + lane) = S[bl + p]
+#pragma unroll
+      for (int p = PW - 1; p >= 0; --p) {
+        if (p < w) {
+          const T xp = __shfl_sync(0xffffffffu, up * il, p);
+          if (lane == p) up = xp;
+          if (lane < p) up = up - S[bl + p] * xp;
+        }
+      }
+      if (lane < w) u[k + lane] = up;
+    }
+    __syncthreads();
+    if (k == 0) break;
+    T xs[PW];
+#pragma unroll
+    for (int p = 0; p < PW; ++p) xs[p] = p < w ? u[k + p] : T(0);
+    for (int j = tid; j < k; j += NT) {
+      const T* col = S + acol(j, C) - j + k;
+      T acc = u[j];
+#pragma unroll
+      for (int p = 0; p < PW; ++p)
+        if (p < w) acc = acc - col[p] * xs[p];
+      u[j] = acc;
+    }
+    __syncthreads();
+  }
+  for (int j = tid; j < C; j += NT) x_out[j] = (double)u[j];
+}
+
 }  // namespace mba

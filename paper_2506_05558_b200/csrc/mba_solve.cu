@@ -57,7 +57,7 @@ constexpr int kUcamStride = 45;  // per free camera: U_aa lower(21) U_af(6) g_a(
 // Optional per-phase cycle counters (build with -DMBA_PHASE_PROF; see
 // paper_2506_05558_b200/build.py --prof). Thread 0 of every CTA accumulates
 // clock64() deltas between phase boundaries; totals land in g_prof[phase].
-enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_JWAIT, PH_JRED, PH_ITEMS, PH_ITEMS2, PH_NCAM, PH_NPAIR, PH_N };
+enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_JWAIT, PH_JRED, PH_ITEMS, PH_ITEMS2, PH_NCAM, PH_NPAIR, PH_BSUB, PH_N };
 #ifdef MBA_PHASE_PROF
 __device__ unsigned long long* g_prof = nullptr;
 #define PROF_DECL __shared__ long long s_prof[PH_N]; long long prof_t = clock64(); \
@@ -950,38 +950,10 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     PROF_MARK(PH_CHOL)
 
     if (!chol_fail) {
-      // column-oriented back substitution D L^T x = y in warp 0 (no
-      // reductions): x_k = u_k / d_k, then u_j -= S[k][j] x_k for j < k
-      if (wid == 0) {
-        constexpr int NU = (6 * MAXC + 1 + 31) / 32;
-        const T* invd = sm.rhs;
-        T u[NU];
-#pragma unroll
-        for (int q = 0; q < NU; ++q) {
-          const int j = lane + 32 * q;
-          u[q] = j < C ? sm.S[acol(j, C) + C - j] : T(0);
-        }
-        for (int k = C - 1; k >= 0; --k) {
-          const int qk = k >> 5;
-          T uk = T(0);
-#pragma unroll
-          for (int q = 0; q < NU; ++q)
-            if (q == qk) uk = __shfl_sync(0xffffffffu, u[q], k & 31);
-          const T xk = uk * invd[k];
-#pragma unroll
-          for (int q = 0; q < NU; ++q) {
-            const int j = lane + 32 * q;
-            if (q == qk && lane == (k & 31)) u[q] = xk;
-            if (j < k) u[q] -= sm.S[acol(j, C) + k - j] * xk;
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < NU; ++q) {
-          const int j = lane + 32 * q;
-          if (j < C) sm.dc[j] = (double)u[q];
-        }
-      }
+      // back substitution D L^T x = y for the cameras (mba_ldl.cuh)
+      ldl_backsub<T, NT>(sm.S, C, sm.rhs, (T*)(smem_raw + L::oTab), sm.dc);
       __syncthreads();
+      PROF_MARK(PH_BSUB)
       // back substitution for the points (miniba.py:217)
       if (opt_pts) {
         const T df = has_f ? T(sm.dc[FI]) : T(0);

@@ -18,7 +18,7 @@ os.environ["MBA_LIB"] = os.environ.get("MBA_PROF_LIB") or os.path.join(REPO, "pa
 # jobs-barrier-wait / job-reduction (grid mode)
 PHASES = ["setup", "cost0", "point", "jobs", "assemble", "cholesky", "solve+backsub", "trials", "commit",
           "ldl|jobs_wait", "jobs_reduce", "setup_stage_validate|cam_chunks_cyc", "setup_slots_X|pair_chunks_cyc",
-          "setup_perm|n_cam_chunks", "setup_pairs|n_pair_chunks"]
+          "setup_perm|n_cam_chunks", "setup_pairs|n_pair_chunks", "camera_backsub"]   # the last: CTA / grid kernels
 
 
 def main():
