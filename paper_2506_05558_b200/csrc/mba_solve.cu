@@ -57,7 +57,7 @@ constexpr int kUcamStride = 45;  // per free camera: U_aa lower(21) U_af(6) g_a(
 // Optional per-phase cycle counters (build with -DMBA_PHASE_PROF; see
 // paper_2506_05558_b200/build.py --prof). Thread 0 of every CTA accumulates
 // clock64() deltas between phase boundaries; totals land in g_prof[phase].
-enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_JWAIT, PH_JRED, PH_ITEMS, PH_ITEMS2, PH_NCAM, PH_NPAIR, PH_BSUB, PH_N };
+enum { PH_SETUP, PH_COST0, PH_POINT, PH_JOBS, PH_ASM, PH_CHOL, PH_SOLVE, PH_TRIAL, PH_COMMIT, PH_JWAIT, PH_JRED, PH_ITEMS, PH_ITEMS2, PH_NCAM, PH_NPAIR, PH_BSUB, PH_JSYNC, PH_N };
 #ifdef MBA_PHASE_PROF
 __device__ unsigned long long* g_prof = nullptr;
 #define PROF_DECL __shared__ long long s_prof[PH_N]; long long prof_t = clock64(); \
@@ -340,6 +340,46 @@ struct GridBufs {
   }
 };
 
+// global (L2) -> shared bulk copy on the TMA engine (cp.async.bulk, 1-D): one
+// thread arms the CTA's mbarrier with the byte count and issues the copies,
+// every thread waits on the barrier's phase. No registers staged (a strided
+// load/store loop waited one L2 round trip per element -- ~50k cycles for the
+// 142 KB reduced system of a 32-camera problem -- and unrolling it cost the
+// grid kernel registers). Sizes are rounded up to 16 bytes: both regions are
+// followed by 16-byte alignment slack. `phase` is the caller's parity bit.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__host__ __device__ constexpr unsigned bulk_bytes(size_t b) { return (unsigned)((b + 15u) & ~size_t(15)); }
+// arm the barrier for `bytes` (the sum of the bulk_bytes of the copies that follow)
+__device__ __forceinline__ void mbar_arm(unsigned long long* mbar, unsigned bytes) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* mbar) {
+  const unsigned mb = smem_u32(mbar);
+  constexpr unsigned kChunk = 32768;
+  for (unsigned off = 0; off < bytes; off += kChunk) {
+    const unsigned sz = bytes - off < kChunk ? bytes - off : kChunk;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32((char*)dst + off)),
+                 "l"((const char*)src + off), "r"(sz), "r"(mb)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(mbar)),
+      "r"(phase)
+      : "memory");
+}
+
 template <typename T, int MAXC, bool RES, bool GRID = false, int NT = kThreads>
 __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) {
   constexpr int kWarps = NT / 32;
@@ -396,6 +436,9 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   sm.blk_a = smem_raw + L::oBlkA;
   sm.blk_b = smem_raw + L::oBlkB;
   __shared__ int s_flag;        // setup error
+  __shared__ __align__(8) unsigned long long s_mbar;   // GRID: bulk copies of the job totals
+  unsigned mbar_phase = 0u;
+  if (GRID && tid == 0) mbar_init(&s_mbar);
   __shared__ int s_C, s_nf;
   double* s_red4 = sm.red;
 
@@ -890,8 +933,18 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
       for (int it2 = gtid; it2 < nu + nb * 36; it2 += gthreads) {
         const int job = it2 < nu ? it2 / kUcamStride : nf + (it2 - nu) / 36;
         const int i = it2 < nu ? it2 % kUcamStride : (it2 - nu) % 36;
+        // the chunk partials in chunk order; eight loads in flight per step
+        // (a job has up to ~25 chunks and each is an L2 round trip)
         T v = T(0);
-        for (int q = coff[job]; q < coff[job + 1]; ++q) v += cpart[(size_t)q * kUcamStride + i];
+        const int q1 = coff[job + 1];
+        for (int q0 = coff[job]; q0 < q1; q0 += 8) {
+          T pv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pv[u] = q0 + u < q1 ? cpart[(size_t)(q0 + u) * kUcamStride + i] : T(0);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (q0 + u < q1) v += pv[u];
+        }
         if (job < nf) {
           U_jobs[job * kUcamStride + i] = v;
         } else {
@@ -904,9 +957,19 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
           }
         }
       }
+      PROF_MARK(PH_JRED)
       gsync();
-      for (int i = tid; i < CA; i += blockDim.x) sm.S[i] = S_jobs[i];
-      for (int i = tid; i < nf * kUcamStride; i += blockDim.x) sm.ucam[i] = U_jobs[i];
+      PROF_MARK(PH_JSYNC)
+      // both jobs' totals into shared memory on the TMA engine (one mbarrier
+      // completion covers both copies)
+      if (tid == 0) {
+        const unsigned bS = bulk_bytes(CA * sizeof(T)), bU = bulk_bytes(nf * kUcamStride * sizeof(T));
+        mbar_arm(&s_mbar, bS + bU);
+        bulk_g2s(sm.S, S_jobs, bS, &s_mbar);
+        bulk_g2s(sm.ucam, U_jobs, bU, &s_mbar);
+      }
+      mbar_wait(&s_mbar, mbar_phase);
+      mbar_phase ^= 1u;
       __syncthreads();
     }
     PROF_MARK(PH_JRED)

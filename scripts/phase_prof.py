@@ -17,8 +17,8 @@ os.environ["MBA_LIB"] = os.environ.get("MBA_PROF_LIB") or os.path.join(REPO, "pa
 # (mba_solve.cu) share 0-8; 9-10 are ldl-core / unused (v4) and
 # jobs-barrier-wait / job-reduction (grid mode)
 PHASES = ["setup", "cost0", "point", "jobs", "assemble", "cholesky", "solve+backsub", "trials", "commit",
-          "ldl|jobs_wait", "jobs_reduce", "setup_stage_validate|cam_chunks_cyc", "setup_slots_X|pair_chunks_cyc",
-          "setup_perm|n_cam_chunks", "setup_pairs|n_pair_chunks", "camera_backsub"]   # the last: CTA / grid kernels
+          "ldl|jobs_wait", "camera_backsub(v4)|jobs_reduce", "setup_stage_validate|cam_chunks_cyc", "setup_slots_X|pair_chunks_cyc",
+          "setup_perm|n_cam_chunks", "setup_pairs|n_pair_chunks", "camera_backsub", "jobs_reduce_sync"]   # the last: CTA / grid kernels
 
 
 def main():
