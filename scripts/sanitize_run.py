@@ -1,6 +1,7 @@
 """Small workloads for compute-sanitizer: the cluster-resident solver (f64 and
 mixed, R = 1, a 16-CTA and a 10-CTA cluster, overflow re-solve), the
-cooperative grid solver (12 cameras), the device pack / sort kernel through
+cooperative grid solver (12 cameras, f64 and mixed), the CTA solver on
+20-camera problems (blocked LDL^T over 15 panels), the device pack / sort kernel through
 lm_solve_batch (shuffled observations), the bootstrap schedule, pose LM,
 triangulation and matching."""
 import os
@@ -31,6 +32,9 @@ def main():
     del os.environ["MBA_V4_ARENA_CAP"]
     grid = make_batch(1, n_cams=12, K=6000, seed=6).problem(0)
     run_device([grid], dict(max_iters=3), "f64", "grid")     # cooperative grid kernel
+    run_device([grid], dict(max_iters=3), "mixed", "grid")
+    wide = make_batch(2, n_cams=20, K=3000, seed=7)               # CTA kernel, 19 free cameras:
+    run_device([wide.problem(i) for i in range(2)], dict(max_iters=3), "f64", "auto")  # 15 LDL panels
     from gsrecon import miniba as M
     from gsrecon.config import CaptureConfig, LmConfig
     from gsrecon.scene import CameraIntrinsics
