@@ -411,8 +411,8 @@ __global__ void __launch_bounds__(NT, 1) bench5(const T* __restrict__ Ain, int C
   for (int i = tid; i < C; i += NT) out[CA + i] = invd[i];
 }
 
-int main() {
-  const int C = 187, CA = C * (C + 3) / 2;
+int main(int argc, char** argv) {
+  const int C = argc > 1 ? atoi(argv[1]) : 187, CA = C * (C + 3) / 2;
   // SPD system: A = B B^T + C I, augmented with a rhs row
   std::vector<double> full((size_t)C * C), B((size_t)C * C), rhs(C);
   srand(1);
