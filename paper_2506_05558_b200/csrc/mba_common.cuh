@@ -190,4 +190,52 @@ __host__ __device__ __forceinline__ int64_t tri_idx(int64_t i, int64_t j) {  // 
   return i * (i + 1) / 2 + j;
 }
 
+template <typename T, int N, int C, int H>
+__device__ __forceinline__ void rs_stage(T (&v)[N], int o, bool up) {
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const T lo = v[i];
+    T hi = T(0);
+    if (H + i < C) hi = v[(H + i) < N ? (H + i) : 0];
+    const T send = up ? lo : hi;
+    const T keep = up ? hi : lo;
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+  }
+}
+
+// Transposed warp reduction of N per-lane values: 5 halving butterfly stages
+// (sum(ceil(N/2^s)) shuffles instead of 5N); the total of value i is written to
+// out[i] by exactly one lane. Fixed order -> bit-reproducible.
+template <typename T, int N, typename F>
+__device__ __forceinline__ void warp_reduce_apply(T (&v)[N], int lane, F&& put) {
+  constexpr int h0 = (N + 1) / 2, h1 = (h0 + 1) / 2, h2 = (h1 + 1) / 2, h3 = (h2 + 1) / 2,
+                h4 = (h3 + 1) / 2;
+  rs_stage<T, N, N, h0>(v, 16, lane & 16);
+  rs_stage<T, N, h0, h1>(v, 8, lane & 8);
+  rs_stage<T, N, h1, h2>(v, 4, lane & 4);
+  rs_stage<T, N, h2, h3>(v, 2, lane & 2);
+  rs_stage<T, N, h3, h4>(v, 1, lane & 1);
+  const int b0 = lane & 1, b1 = (lane >> 1) & 1, b2 = (lane >> 2) & 1, b3 = (lane >> 3) & 1,
+            b4 = (lane >> 4) & 1;
+#pragma unroll
+  for (int j = 0; j < h4; ++j) {
+    int i = j + b0 * h4;
+    if (i >= h3) continue;
+    i += b1 * h3;
+    if (i >= h2) continue;
+    i += b2 * h2;
+    if (i >= h1) continue;
+    i += b3 * h1;
+    if (i >= h0) continue;
+    i += b4 * h0;
+    if (i >= N) continue;
+    put(i, v[j]);
+  }
+}
+template <typename T, int N>
+__device__ __forceinline__ void warp_reduce_to(T (&v)[N], T* out, int lane) {
+  warp_reduce_apply(v, lane, [out](int i, T x) { out[i] = x; });
+}
+
+
 }  // namespace mba

@@ -860,12 +860,10 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
             }
           }
         }
-#pragma unroll
-        for (int i = 0; i < kUcamStride; ++i) acc[i] = warp_sum(acc[i]);
+        // transposed warp reduction (halving butterflies, ~N shuffles instead
+        // of 5N); one lane writes each total
         T* dst = GRID ? cpart + (size_t)item * kUcamStride : U_jobs + s * kUcamStride;
-#pragma unroll
-        for (int i = 0; i < kUcamStride; ++i)
-          if ((i & 31) == lane) dst[i] = acc[i];
+        warp_reduce_to<T, kUcamStride>(acc, dst, lane);
       } else {
         const int blk = job - nf;
         const int sa = sm.blk_a[blk], sb = sm.blk_b[blk];
@@ -902,27 +900,19 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
               acc[r * 6 + cc] += yi[r * 3] * yj[cc * 3] + yi[r * 3 + 1] * yj[cc * 3 + 1] +
                                  yi[r * 3 + 2] * yj[cc * 3 + 2];
         }
-#pragma unroll
-        for (int i = 0; i < 36; ++i) acc[i] = warp_sum(acc[i]);
         if constexpr (GRID) {
-          T* dst = cpart + (size_t)item * kUcamStride;
-#pragma unroll
-          for (int i = 0; i < 36; ++i)
-            if ((i & 31) == lane) dst[i] = acc[i];
+          warp_reduce_to<T, 36>(acc, cpart + (size_t)item * kUcamStride, lane);
         } else {
-          // acc[r][cc] = S(6sa + r, 6sb + cc); stored in the lower triangle, lanes
-          // writing disjoint entries
-#pragma unroll
-          for (int i = 0; i < 36; ++i) {
-            if ((i & 31) != lane) continue;
+          // acc[r][cc] = S(6sa + r, 6sb + cc); stored in the lower triangle
+          warp_reduce_apply(acc, lane, [&](int i, T v) {
             const int r = i / 6, cc = i % 6;
             if (sa == sb) {
-              if (cc <= r) S_jobs[acol(6 * sa + cc, C) + r - cc] = -acc[i];
+              if (cc <= r) S_jobs[acol(6 * sa + cc, C) + r - cc] = -v;
             } else {
               const int row = 6 * sb + cc, col = 6 * sa + r;
-              S_jobs[acol(col, C) + row - col] = -acc[i];
+              S_jobs[acol(col, C) + row - col] = -v;
             }
-          }
+          });
         }
       }
 #ifdef MBA_PHASE_PROF

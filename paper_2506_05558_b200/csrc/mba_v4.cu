@@ -159,49 +159,6 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
-template <typename T, int N, int C, int H>
-__device__ __forceinline__ void rs_stage(T (&v)[N], int o, bool up) {
-#pragma unroll
-  for (int i = 0; i < H; ++i) {
-    const T lo = v[i];
-    T hi = T(0);
-    if (H + i < C) hi = v[(H + i) < N ? (H + i) : 0];
-    const T send = up ? lo : hi;
-    const T keep = up ? hi : lo;
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-  }
-}
-
-// Transposed warp reduction of N per-lane values: 5 halving butterfly stages
-// (sum(ceil(N/2^s)) shuffles instead of 5N); the total of value i is written to
-// out[i] by exactly one lane. Fixed order -> bit-reproducible.
-template <typename T, int N>
-__device__ __forceinline__ void warp_reduce_to(T (&v)[N], T* out, int lane) {
-  constexpr int h0 = (N + 1) / 2, h1 = (h0 + 1) / 2, h2 = (h1 + 1) / 2, h3 = (h2 + 1) / 2,
-                h4 = (h3 + 1) / 2;
-  rs_stage<T, N, N, h0>(v, 16, lane & 16);
-  rs_stage<T, N, h0, h1>(v, 8, lane & 8);
-  rs_stage<T, N, h1, h2>(v, 4, lane & 4);
-  rs_stage<T, N, h2, h3>(v, 2, lane & 2);
-  rs_stage<T, N, h3, h4>(v, 1, lane & 1);
-  const int b0 = lane & 1, b1 = (lane >> 1) & 1, b2 = (lane >> 2) & 1, b3 = (lane >> 3) & 1,
-            b4 = (lane >> 4) & 1;
-#pragma unroll
-  for (int j = 0; j < h4; ++j) {
-    int i = j + b0 * h4;
-    if (i >= h3) continue;
-    i += b1 * h3;
-    if (i >= h2) continue;
-    i += b2 * h2;
-    if (i >= h1) continue;
-    i += b3 * h1;
-    if (i >= h0) continue;
-    i += b4 * h0;
-    if (i >= N) continue;
-    out[i] = v[j];
-  }
-}
-
 // Deterministic block sum of N doubles (result to every thread).
 template <int NW, int N>
 __device__ __forceinline__ void block_sum_d(double (&v)[N], double* red) {
@@ -1289,6 +1246,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
         if (lane + 32 < C) { dc[lane + 32] = (double)u1; dcT[lane + 32] = u1; }
       }
       __syncthreads();
+      PROF_MARK(PH_CHB)
       // trial cameras of all five tries (R <- exp(frac dw) R, t + frac dt,
       // miniba.py:264-266), by the highest-numbered threads, overlapped with
       // the point back substitution (the barrier after it publishes both)
