@@ -68,8 +68,11 @@ class OutputGather:
     def __init__(self, torch, dist, local, max_iters, device, comm_device=None, dst=0, traces=True,
                  group=None):
         self.torch, self.dist, self.dst, self.group = torch, dist, dst, group
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        # with a process group the gather always runs the collective (also at
+        # world size 1); without one the outputs are returned in place
+        self.collective = dist is not None and dist.is_initialized()
+        self.world = dist.get_world_size(group) if self.collective else 1
+        self.rank = dist.get_rank(group) if self.collective else 0
         self.max_iters, self.traces = max_iters, traces
         self.device = device
         self.comm = comm_device or device
@@ -86,7 +89,7 @@ class OutputGather:
         u8 = dict(dtype=torch.uint8, device=self.comm)
         self.send = torch.zeros(self.nbytes, **u8)
         self.recv = ([torch.zeros(self.nbytes, **u8) for _ in range(self.world)]
-                     if self.rank == dst and self.world > 1 else None)
+                     if self.rank == dst and self.collective else None)
 
     @property
     def bytes_per_step(self):
@@ -107,7 +110,7 @@ class OutputGather:
 
     def gather(self, outputs):
         torch = self.torch
-        if self.world == 1:
+        if not self.collective:
             return {name: self._get(outputs, name).reshape(-1)[:n] for name, n in self.counts[0].items()}
         self.pack(outputs)
         if self.comm != self.device:
