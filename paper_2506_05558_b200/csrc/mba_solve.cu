@@ -327,7 +327,8 @@ struct GridBufs {
   static constexpr size_t oU = align16(oS + sizeof(T) * CA);          // T[MAXC][kUcamStride]
   static constexpr size_t oCnt = align16(oU + sizeof(T) * MAXC * kUcamStride);  // int[MAXC + NB + 2]
   static constexpr size_t oCoff = align16(oCnt + 4 * (MAXC + NB + 2));  // int[MAXC + NB + 1] chunks per job
-  static constexpr size_t oRed = align16(oCoff + 4 * (MAXC + NB + 1));  // double[2][G][4]
+  static constexpr size_t oJobQ = align16(oCoff + 4 * (MAXC + NB + 1));  // int[2] job-chunk queues (by LM iteration parity)
+  static constexpr size_t oRed = align16(oJobQ + 8);                   // double[2][G][4]
   static __host__ __device__ size_t oChunk(int G) { return align16(oRed + 8 * 2 * 4 * (size_t)G); }  // int2[chunks]
   static __host__ __device__ size_t oPart(int G, int64_t chunks) {   // T[chunks][kUcamStride]
     return align16(oChunk(G) + 8 * (size_t)chunks);
@@ -468,6 +469,8 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
   const Scratch<T, RES> W = scratch_at<T, RES>(
       RES ? smem_raw + L::kFixed : P.ws + (GRID ? 0 : (size_t)blockIdx.x * P.ws_slot_bytes), D);
   int* gcnt = GRID ? (int*)(P.grid + GB::oCnt) : nullptr;
+  int* jobq = GRID ? (int*)(P.grid + GB::oJobQ) : nullptr;
+  if (GRID && rank == 0 && tid == 0) jobq[0] = jobq[1] = 0;   // published by the setup's grid syncs
   constexpr int YSTR = YS<RES>::v;
   auto ld18 = [](const T* p, T y[18]) {
     if constexpr (RES && sizeof(T) == 4) load18v2((const float*)p, (float*)y); else load18(p, y);
@@ -799,7 +802,18 @@ __device__ void solve_one(const SolveParams& P, int b, unsigned char* smem_raw) 
     T* S_jobs = GRID ? (T*)(P.grid + GB::oS) : sm.S;
     T* U_jobs = GRID ? (T*)(P.grid + GB::oU) : sm.ucam;
     const int n_items = GRID ? coff[nf + nb] : nf + nb;
-    for (int item = gwid; item < n_items; item += gwarps) {
+    // cooperative mode: warps pull chunks from a grid-wide queue (one atomic per
+    // chunk; results do not depend on which warp takes which chunk) -- the
+    // static round robin left warps with 1 or 2 chunks of unequal cost waiting
+    // at the grid barrier
+    if (GRID && rank == 0 && tid == 0) jobq[(it + 1) & 1] = 0;   // last used two iterations ago
+    for (int item = gwid;; item += gwarps) {
+      if constexpr (GRID) {
+        int q = 0;
+        if (lane == 0) q = atomicAdd(jobq + (it & 1), 1);
+        item = __shfl_sync(0xffffffffu, q, 0);
+      }
+      if (item >= n_items) break;
       // reconverge the warp before the lane-strided loops: without it the lanes
       // that left the previous item's loop at different trip counts stay
       // split and the loop runs with ~2 of 32 lanes active (measured)
