@@ -239,7 +239,17 @@ __device__ __forceinline__ int block_factor(T a[PW], int w, int lane, int k, T* 
 #pragma unroll
       for (int c = p + 1; c < PW; ++c) wc[c] = __shfl_sync(0xffffffffu, a[p], c);
       bad |= !(d > T(0)) || !isfinite((double)d);
-      const T inv = BF == 1 ? __drcp_rn(d) : T(1) / d;
+      T inv;
+      if constexpr (BF == 3) {
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"((double)d));
+        double e = fma(-(double)d, r, 1.0);
+        r = fma(r, e, r);
+        e = fma(-(double)d, r, 1.0);
+        inv = (T)fma(r, e, r);
+      } else {
+        inv = BF == 1 ? __drcp_rn(d) : T(1) / d;
+      }
       const T l = a[p] * inv;
 #pragma unroll
       for (int c = p + 1; c < PW; ++c)
@@ -490,6 +500,7 @@ int main(int argc, char** argv) {
   run(bench<double, 2>, "V2 lane=row, scalar L loads");
   run(bench5<double, 0>, "V5 lookahead, unrolled, interior fast path");
   run(bench5<double, 0, 2>, "V6 = V5 with 2 rows per lane");
+  run(bench5<double, 3>, "V5 + MUFU-seeded Newton reciprocal");
   run(bench<double, 3>, "V3 calibration (no L loads, wrong result)");
   return 0;
 }
