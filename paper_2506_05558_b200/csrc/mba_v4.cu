@@ -812,6 +812,21 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     for (int i = 0; i < 4; ++i) out[i] = acc[i];
   };
 
+  // Linearisation cache (when the arena has room): per point the undamped
+  // V_p, g_p, Wf_p and per thread its focal partials. An iteration that
+  // follows a rejected one re-linearises at unchanged parameters (the
+  // reference rebuilds the same system with a larger lambda, miniba.py:
+  // 223-296), so its point pass only re-damps and re-factorises (40 % of
+  // config-4 iterations are full rejections on the plateau). Same values,
+  // same order -> results bit-identical to recomputing.
+  constexpr int VCS = 13;   // 12 values per point, odd stride
+  T* vcache = reinterpret_cast<T*>(
+      reinterpret_cast<unsigned char*>(pairs) + al16(4 * (size_t)(overflow ? 0 : s_npairs)));
+  T* pcache = vcache + (size_t)VCS * nlp;   // [NT][2]
+  const bool cache_ok = !overflow && fixed_need + al16(4 * (size_t)s_npairs) +
+                                         sizeof(T) * ((size_t)VCS * nlp + 2 * NT) <= P.arena;
+  bool reuse = false;
+
   double* costs = O.costs + (size_t)b * (max_it + 1);
   double* lambdas = O.lambdas + (size_t)b * max_it;
   uint8_t* accepted = O.accepted + (size_t)b * max_it;
@@ -834,12 +849,26 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
     const T inv_f = T(1.0 / f);
     // ---------- point pass: compact Jacobians, V_p / g_p / Wf_p, point factor ----------
     T part[4] = {T(0), T(0), T(0), T(0)};  // U_ff, g_f, sum yf.yf, sum yf.z
+    if (reuse) {
+      part[0] = pcache[2 * tid];
+      part[1] = pcache[2 * tid + 1];
+    }
     for (int sl = tid; sl < nlp; sl += NT) {
       const double Xp[3] = {Xs[3 * sl], Xs[3 * sl + 1], Xs[3 * sl + 2]};
       T V[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};  // 00 10 11 20 21 22
       T g[3] = {T(0), T(0), T(0)}, wf[3] = {T(0), T(0), T(0)};
       const int j0 = ptr[sl], j1 = ptr[sl + 1];
-      for (int kl = j0; kl < j1; ++kl) {
+      T* vc = vcache + (size_t)sl * VCS;
+      if (reuse) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) V[i] = vc[i];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          g[i] = vc[6 + i];
+          wf[i] = vc[9 + i];
+        }
+      }
+      for (int kl = reuse ? j1 : j0; kl < j1; ++kl) {
         const float4 o = sobs[kl];
         const int c = __float_as_int(o.z);
         double uu, vv;
@@ -873,6 +902,15 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
             for (int q = 0; q < 3; ++q) wf[q] += B0[q] * cj.F0 + B1[q] * cj.F1;
         }
       }
+      if (cache_ok && !reuse) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) vc[i] = V[i];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          vc[6 + i] = g[i];
+          vc[9 + i] = wf[i];
+        }
+      }
       if (!opt_pts) continue;
       // damping (miniba.py:191-193) and 3x3 Cholesky of Vd
       V[0] += tlam * (V[0] > T(kDiagFloor) ? V[0] : T(kDiagFloor));
@@ -894,6 +932,10 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       pw[0] = i00; pw[1] = L10; pw[2] = i11; pw[3] = L20; pw[4] = L21; pw[5] = i22;
       pw[6] = z0; pw[7] = z1; pw[8] = z2;
       pw[9] = f0; pw[10] = f1; pw[11] = f2;
+    }
+    if (cache_ok && !reuse) {
+      pcache[2 * tid] = part[0];
+      pcache[2 * tid + 1] = part[1];
     }
     {  // this CTA's focal partials
       double pd[4] = {(double)part[0], (double)part[1], (double)part[2], (double)part[3]};
@@ -1437,6 +1479,7 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
       }
     }
     if (lead) costs[it + 1] = cur;
+    reuse = cache_ok && took < 0;   // parameters unchanged: the next linearisation is this one
     ++it;
     __syncthreads();
     PROF_MARK(PH_COMMIT)
