@@ -1296,7 +1296,7 @@ static int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutput
     // plan are re-solved by the CTA kernel (restricted to flagged problems)
     const int R = v4::plan_cluster(d, cfg);
     if (R > 0) {
-      int rc = v4::launch(d, cfg, o, st, R);
+      int rc = v4::launch(d, cfg, o, st, R, ws, ws_bytes);
       if (rc != MBA_OK || !v4::may_overflow(d, cfg)) return rc;
       return launch_cfg<T, 8, false>(d, cfg, o, ws, ws_bytes, st, 1);
     }

@@ -145,6 +145,9 @@ struct Params {
   MbaLmConfig cfg;
   MbaOutputs o;
   size_t arena;   // bytes of dynamic shared memory after the fixed part
+  unsigned char* gcache;   // optional per-SM linearisation caches (one CTA per SM plans)
+  size_t gcache_slot;      // bytes per SM
+  int gcache_slots;        // number of SM slots
 };
 
 // ---------------------------------------------------------------------------
@@ -823,8 +826,20 @@ __device__ void solve_problem(const Params& P, unsigned char* smem) {
   T* vcache = reinterpret_cast<T*>(
       reinterpret_cast<unsigned char*>(pairs) + al16(4 * (size_t)(overflow ? 0 : s_npairs)));
   T* pcache = vcache + (size_t)VCS * nlp;   // [NT][2]
-  const bool cache_ok = !overflow && fixed_need + al16(4 * (size_t)s_npairs) +
-                                         sizeof(T) * ((size_t)VCS * nlp + 2 * NT) <= P.arena;
+  bool cache_ok = !overflow && fixed_need + al16(4 * (size_t)s_npairs) +
+                                   sizeof(T) * ((size_t)VCS * nlp + 2 * NT) <= P.arena;
+  if (!cache_ok && !overflow && P.gcache != nullptr) {
+    // no room in shared memory (fp64): the slot of this SM in global memory
+    // (L2-resident; one point's 12 values are one round trip). Only plans with
+    // one CTA per SM pass gcache, so the slot has a single owner.
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if ((int)smid < P.gcache_slots && sizeof(T) * ((size_t)VCS * nlp + 2 * NT) <= P.gcache_slot) {
+      vcache = reinterpret_cast<T*>(P.gcache + (size_t)smid * P.gcache_slot);
+      pcache = vcache + (size_t)VCS * nlp;
+      cache_ok = true;
+    }
+  }
   bool reuse = false;
 
   double* costs = O.costs + (size_t)b * (max_it + 1);
@@ -1639,7 +1654,8 @@ static Plan plan_t(const MbaBatchDesc* d) {
 }
 
 template <typename T, int R, int NT, int MINB>
-static int launch_t(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st) {
+static int launch_t(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st,
+                    void* ws, size_t ws_bytes) {
   auto kern = solve_v4_kernel<T, R, NT, MINB>;
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return MBA_ERR_CUDA;
@@ -1658,6 +1674,20 @@ static int launch_t(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutp
   P.cfg = *cfg;
   P.o = *o;
   P.arena = smem - Fixed<T>::kBytes;
+  P.gcache = nullptr;
+  P.gcache_slot = 0;
+  P.gcache_slots = 0;
+  if (MINB == 1 && ws != nullptr) {   // one CTA per SM: per-SM linearisation caches in the workspace
+    int dev = 0, n_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const size_t slot = al16(sizeof(T) * (13 * (size_t)d->max_points + 2 * NT));
+    if (n_sm > 0 && slot * (size_t)n_sm <= ws_bytes) {
+      P.gcache = static_cast<unsigned char*>(ws);
+      P.gcache_slot = slot;
+      P.gcache_slots = n_sm;
+    }
+  }
   if (const char* e = getenv("MBA_V4_ARENA_CAP")) {   // tests: force the overflow re-solve path
     const size_t cap = (size_t)atol(e);
     if (cap < P.arena) P.arena = cap;
@@ -1687,35 +1717,35 @@ static int launch_t(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutp
 
 template <typename T>
 static int launch_prec(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st,
-                       const Plan& p) {
+                       const Plan& p, void* ws, size_t ws_bytes) {
   if (getenv("MBA_DEBUG")) fprintf(stderr, "mba v4 plan: R=%d NT=%d per_sm=%d\n", p.R, p.nt, p.per_sm);
   if (p.per_sm == 2) {
     if (p.nt == 128) {
       switch (p.R) {
-        case 1: return launch_t<T, 1, 128, 2>(d, cfg, o, st);
-        case 2: return launch_t<T, 2, 128, 2>(d, cfg, o, st);
-        case 4: return launch_t<T, 4, 128, 2>(d, cfg, o, st);
+        case 1: return launch_t<T, 1, 128, 2>(d, cfg, o, st, ws, ws_bytes);
+        case 2: return launch_t<T, 2, 128, 2>(d, cfg, o, st, ws, ws_bytes);
+        case 4: return launch_t<T, 4, 128, 2>(d, cfg, o, st, ws, ws_bytes);
       }
     } else if constexpr (sizeof(T) == 4) {
       switch (p.R) {
-        case 1: return launch_t<T, 1, 256, 2>(d, cfg, o, st);
-        case 2: return launch_t<T, 2, 256, 2>(d, cfg, o, st);
-        case 4: return launch_t<T, 4, 256, 2>(d, cfg, o, st);
+        case 1: return launch_t<T, 1, 256, 2>(d, cfg, o, st, ws, ws_bytes);
+        case 2: return launch_t<T, 2, 256, 2>(d, cfg, o, st, ws, ws_bytes);
+        case 4: return launch_t<T, 4, 256, 2>(d, cfg, o, st, ws, ws_bytes);
       }
     }
     return MBA_ERR_TOO_LARGE;
   }
-  if (p.nt == 512 && p.R == 1) return launch_t<T, 1, 512, 1>(d, cfg, o, st);
-  if (p.nt == 384 && p.R == 1) return launch_t<T, 1, 384, 1>(d, cfg, o, st);
+  if (p.nt == 512 && p.R == 1) return launch_t<T, 1, 512, 1>(d, cfg, o, st, ws, ws_bytes);
+  if (p.nt == 384 && p.R == 1) return launch_t<T, 1, 384, 1>(d, cfg, o, st, ws, ws_bytes);
   switch (p.R) {
-    case 1: return launch_t<T, 1, 256, 1>(d, cfg, o, st);
-    case 2: return launch_t<T, 2, 256, 1>(d, cfg, o, st);
-    case 4: return launch_t<T, 4, 256, 1>(d, cfg, o, st);
-    case 8: return launch_t<T, 8, 256, 1>(d, cfg, o, st);
-    case 9: return launch_t<T, 9, 256, 1>(d, cfg, o, st);
-    case 10: return launch_t<T, 10, 256, 1>(d, cfg, o, st);
-    case 12: return launch_t<T, 12, 256, 1>(d, cfg, o, st);
-    case 16: return launch_t<T, 16, 256, 1>(d, cfg, o, st);
+    case 1: return launch_t<T, 1, 256, 1>(d, cfg, o, st, ws, ws_bytes);
+    case 2: return launch_t<T, 2, 256, 1>(d, cfg, o, st, ws, ws_bytes);
+    case 4: return launch_t<T, 4, 256, 1>(d, cfg, o, st, ws, ws_bytes);
+    case 8: return launch_t<T, 8, 256, 1>(d, cfg, o, st, ws, ws_bytes);
+    case 9: return launch_t<T, 9, 256, 1>(d, cfg, o, st, ws, ws_bytes);
+    case 10: return launch_t<T, 10, 256, 1>(d, cfg, o, st, ws, ws_bytes);
+    case 12: return launch_t<T, 12, 256, 1>(d, cfg, o, st, ws, ws_bytes);
+    case 16: return launch_t<T, 16, 256, 1>(d, cfg, o, st, ws, ws_bytes);
     default: return MBA_ERR_TOO_LARGE;
   }
 }
@@ -1751,10 +1781,10 @@ int V4_ENTRY(may_overflow)(const MbaBatchDesc* d) {
 }
 
 int V4_ENTRY(launch)(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st,
-                     int R) {
+                     int R, void* ws, size_t ws_bytes) {
   const Plan p = plan_t<TU>(d);
   if (p.R != R || R == 0) return MBA_ERR_TOO_LARGE;
-  return launch_prec<TU>(d, cfg, o, st, p);
+  return launch_prec<TU>(d, cfg, o, st, p, ws, ws_bytes);
 }
 
 }  // namespace v4

@@ -20,8 +20,10 @@ constexpr int kStatusPlanOverflow = -2;
 // are the per-type entry points, dispatched below on cfg->precision.
 int plan_cluster_f64(const MbaBatchDesc* d);
 int plan_cluster_f32(const MbaBatchDesc* d);
-int launch_f64(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st, int R);
-int launch_f32(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st, int R);
+int launch_f64(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st, int R,
+               void* ws, size_t ws_bytes);
+int launch_f32(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st, int R,
+               void* ws, size_t ws_bytes);
 int may_overflow_f64(const MbaBatchDesc* d);
 int may_overflow_f32(const MbaBatchDesc* d);
 #ifdef MBA_PHASE_PROF
@@ -40,11 +42,14 @@ inline int plan_cluster(const MbaBatchDesc* d, const MbaLmConfig* cfg) {
 
 // Launch the solver; returns MBA_OK / negative MbaStatus. Problems that do not
 // fit report kStatusPlanOverflow (the caller then runs the CTA kernel
-// restricted to those problems).
+// restricted to those problems). `ws` (optional, the mba_solve workspace)
+// holds the per-SM linearisation caches of plans whose shared memory has no
+// room for them.
 inline int launch(const MbaBatchDesc* d, const MbaLmConfig* cfg, const MbaOutputs* o, cudaStream_t st,
-                  int cluster) {
+                  int cluster, void* ws = nullptr, size_t ws_bytes = 0) {
   if (plan_cluster(d, cfg) != cluster || cluster == 0) return MBA_ERR_TOO_LARGE;
-  return cfg->precision == MBA_LIN_F64 ? launch_f64(d, cfg, o, st, cluster) : launch_f32(d, cfg, o, st, cluster);
+  return cfg->precision == MBA_LIN_F64 ? launch_f64(d, cfg, o, st, cluster, ws, ws_bytes)
+                                       : launch_f32(d, cfg, o, st, cluster, ws, ws_bytes);
 }
 
 // 0 when no problem of the batch can exceed the plan (one CTA per problem and
