@@ -164,7 +164,9 @@ int32_t mba_compact_traces(int32_t n_problems, int32_t max_iters, const int32_t*
 
 int32_t mba_abi_version(void);
 
-/* Bytes of device workspace mba_solve needs for this batch and config. */
+/* Bytes of device workspace mba_solve needs for this batch and config (scratch
+ * of the CTA kernel and the cooperative grid buffers; the cluster kernel also
+ * keeps per-SM linearisation caches in it when it is large enough). */
 size_t mba_workspace_bytes(const MbaBatchDesc* desc, const MbaLmConfig* cfg);
 
 /* Full Levenberg-Marquardt mini-BA on every problem of the batch: replaces
@@ -177,8 +179,9 @@ int32_t mba_solve(const MbaBatchDesc* desc, const MbaLmConfig* cfg, const MbaOut
 
 /* Which device path mba_solve takes for this batch and config: the cluster
  * size R > 0 of the cluster-resident kernel (R CTAs per problem, all scratch in
- * shared memory; fused backtracking tries 1-4), or -1 warp-per-problem, -2 CTA
- * per problem, -3 point-wise, -4 whole-GPU cooperative; 0 = not solvable. */
+ * shared memory; fused backtracking tries 1-4), or -2 CTA per problem (9-32
+ * cameras, overflow re-solves), -4 whole-GPU cooperative (a few large
+ * problems); 0 = not solvable (more than 32 cameras: the stage kernels). */
 int32_t mba_solve_plan(const MbaBatchDesc* desc, const MbaLmConfig* cfg);
 
 /* Number of kernel launches one mba_solve call issues for this batch and config

@@ -312,7 +312,7 @@ def _desc(db, prm):
 
 def plan(db: DeviceBatch, prm: LmParams) -> int:
     """Device path mba_solve takes (mba_solve_plan): cluster size R > 0 of the
-    cluster-resident kernel, or -1 warp / -2 CTA / -3 point-wise / -4 grid."""
+    cluster-resident kernel, or -2 CTA kernel / -4 cooperative grid kernel."""
     d, c = _desc(db, prm)
     return int(_lib.lib().mba_solve_plan(ct.byref(d), ct.byref(c)))
 
