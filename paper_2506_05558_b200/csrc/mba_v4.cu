@@ -50,11 +50,15 @@ namespace cg = cooperative_groups;
 namespace mba {
 namespace v4 {
 
+// observations per thread in flight in the cost passes (try 0 / fused tries
+// 1-4). One: the passes are not latency-bound enough for unrolling to pay for
+// its registers (scripts/gpu/cost_u_sweep*.sh, config 4: f64 259k at 4 / 2 ->
+// 266k at 1 / 1, mixed 297k -> 312k).
 #ifndef MBA_COST_U
-#define MBA_COST_U 4
+#define MBA_COST_U 1
 #endif
 #ifndef MBA_COST4_U
-#define MBA_COST4_U 2
+#define MBA_COST4_U 1
 #endif
 constexpr int NW_MAX = 16;                       // layout bound: warps per CTA
 constexpr int MAXN = 8;                          // cameras per problem

@@ -1,0 +1,15 @@
+# config-4 f64 throughput vs the cost-pass unroll factors (MBA_COST_U / MBA_COST4_U)
+F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr"
+C=paper_2506_05558_b200/csrc
+if [ -n "${CU_LIST:-}" ]; then IFS=, read -ra LIST <<< "$CU_LIST"; else LIST=("4 2" "2 2" "8 2" "4 1" "4 4"); fi
+rm -rf /tmp/objs; mkdir -p /tmp/objs
+(for s in mba_solve mba_stages mba_pose mba_tri mba_match mba_pack mba_bootstrap; do
+   /usr/local/cuda/bin/nvcc $F -c $C/$s.cu -o /tmp/objs/$s.o & done;
+ /usr/local/cuda/bin/nvcc $F -DMBA_V4_F32 -c $C/mba_v4.cu -o /tmp/objs/mba_v4_f32.o & wait)
+for cu in "${LIST[@]}"; do
+  set -- $cu
+  /usr/local/cuda/bin/nvcc $F -DMBA_COST_U=$1 -DMBA_COST4_U=$2 -c $C/mba_v4.cu -o /tmp/mba_v4_f64.o
+  /usr/local/cuda/bin/nvcc -shared -gencode arch=compute_100a,code=sm_100a -o /tmp/libminiba_u.so /tmp/mba_v4_f64.o /tmp/objs/*.o -lcudart
+  MBA_LIB=/tmp/libminiba_u.so python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | \
+    python -c "import json,sys;d=json.loads(sys.stdin.read());print('U=$1 U4=$2', round(d['value']))"
+done
