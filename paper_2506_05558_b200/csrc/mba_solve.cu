@@ -213,7 +213,7 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane) {
 }
 
 // Cost pass over all observations with camera set (Rs, ts, f) and points
-// X + frac * dp. Four observations per thread are in flight at once.
+// X + frac * dp (MBA_GRID_COST_U observations per thread per step).
 // Returns (sum rho, sum e, sum e^2) to every thread.
 template <typename T>
 __device__ void cost_pass(const MbaObs* __restrict__ obs, const float* __restrict__ lo, int K,
@@ -221,7 +221,10 @@ __device__ void cost_pass(const MbaObs* __restrict__ obs, const float* __restric
                           bool use_dp, const double* Rs, const double* ts, double f, double cx,
                           double cy, double delta, int loss, double* red, double out[3],
                           int start, int stride) {
-  constexpr int U = 4;
+#ifndef MBA_GRID_COST_U
+#define MBA_GRID_COST_U 1   // config 5: 15.5 ms at 4, 15.4 at 2, 15.1 at 1 (scripts/gpu/grid_cost_u.sh)
+#endif
+  constexpr int U = MBA_GRID_COST_U;
   double acc[3] = {0.0, 0.0, 0.0};
   for (int k0 = start; k0 < K; k0 += U * stride) {
     Obs o[U];
