@@ -1,6 +1,6 @@
-"""Per-phase cycle breakdown of mba::solve_kernel (profiling build).
+"""Per-phase cycle breakdown of the solver kernels (profiling build of
+libminiba, -DMBA_PHASE_PROF; rebuilt here when a source is newer).
 
-    python paper_2506_05558_b200/build.py --prof
     python scripts/phase_prof.py --config 4 --problems 8192 [--precision mixed]
 """
 import argparse
@@ -11,7 +11,21 @@ import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [REPO, os.path.join(REPO, "src")]
-os.environ["MBA_LIB"] = os.environ.get("MBA_PROF_LIB") or os.path.join(REPO, "paper_2506_05558_b200", "libminiba_prof.so")
+_PROF = os.path.join(REPO, "paper_2506_05558_b200", "libminiba_prof.so")
+os.environ["MBA_LIB"] = os.environ.get("MBA_PROF_LIB") or _PROF
+
+
+def _ensure_prof_lib():
+    """Rebuild the profiling library when any CUDA source is newer (a stale
+    one silently reports the previous code's phases)."""
+    if os.environ.get("MBA_PROF_LIB"):
+        return
+    csrc = os.path.join(REPO, "paper_2506_05558_b200", "csrc")
+    srcs = [os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith((".cu", ".cuh"))]
+    if os.path.exists(_PROF) and all(os.path.getmtime(f) <= os.path.getmtime(_PROF) for f in srcs):
+        return
+    from paper_2506_05558_b200 import build
+    build.build(prof=True)
 
 # index -> phase; the cluster kernel (mba_v4.cu) and the CTA / grid kernels
 # (mba_solve.cu) share 0-8; 9-10 are ldl-core / unused (v4) and
@@ -28,6 +42,7 @@ def main():
     ap.add_argument("--precision", default="mixed")
     ap.add_argument("--kernel", default="auto")
     a = ap.parse_args()
+    _ensure_prof_lib()
     import torch
     from paper_2506_05558_b200 import _lib, solver
     from paper_2506_05558_b200.synth import CONFIGS, make_batch
